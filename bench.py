@@ -1,0 +1,427 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 positional population count (driver contract).
+
+Default (N=1): BASELINE.json configs[1] = C2, w=8 over a 1 GiB array of
+Bernoulli(0.5) bits generated in place in HBM.  One step = one pass of the
+hot path (pp_count, one launch of the sm_100a kernel) over the whole array;
+under torchrun (N>1) each rank counts its own 1 GiB shard of an N GiB array
+(weak scaling) and each step ends with the NCCL allreduce of the counters.
+
+Printed JSON keys beyond the base contract:
+  roofline      dominant kernel: algorithmic bytes per launch (n input bytes,
+                SURVEY.md 8d) / mean launch time vs MEASURED_PEAKS.hbm_gbs
+  cpu_baseline  the reference's fastest CPU path (C restatement of
+                NumbaKernel.run, oracle/) on the host's cores, bounded sample
+  e2e           the same metric through the public API pospopcnt() on a
+                pinned HOST buffer: H2D copies + D2H of the counters inside
+                the timed region
+  exact         counters after all steps == steps x CPU oracle (C2 only)
+
+``--impl reference`` times the reference's CPU implementation (the oracle
+port; the reference itself is Python and is not on the GPU box) on the same
+config with all host threads.  ``--config`` selects another BASELINE config
+(c1, c3, c4, c4seg, c5) for an extra line; ``--sweep`` prints one line per
+word width.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "pospopcnt input GB/s (fraction of HBM peak) at 1/2/4/8 B200, per word width"
+GIB = 1 << 30
+MIB = 1 << 20
+
+CONFIGS = {
+    # name: (generator, width, bytes per GPU, description)
+    "c1": ("uniform", 16, 2 * MIB, "w=16, 2 MiB, Bernoulli(0.5), aligned"),
+    "c2": ("uniform", 8, GIB, "w=8, 1 GiB, Bernoulli(0.5)"),
+    "c3": ("onehot32", 32, 4 * GIB, "w=32 one-hot, 4 GiB, bounded Zipf(1.1) over 32 bits"),
+    "c4": ("bernoulli", 64, 64 * MIB, "w=64, 64 MiB at byte offset 3, Bernoulli(0.01)"),
+    "c4seg": ("bernoulli", 64, GIB, "w=64, 262,144 segments x 4 KiB, Bernoulli(0.01)"),
+    "c5": ("blocks", 16, 8 * GIB, "w=16, 8 GiB shard per GPU of the 64 GiB array, "
+                                  "Bernoulli(p) with p ~ U[0,1] per 1 MiB block"),
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def load_traffic(kernel_key):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(kernel_key)
+    except Exception:  # noqa: BLE001
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------ CPU legs
+
+def time_cpu_port(host_u8, w, min_time):
+    """Reference harness methodology (bench.py:124-160): k doubles until a
+    round lasts >= min_time, >= 2 rounds, report the last.  Returns
+    (GB/s, threads, counters of one pass, k, seconds)."""
+    from oracle import oracle as O
+    n = host_u8.size
+    threads = host_threads()
+    once = O.hs512(host_u8, 0, n, w, threads=threads)  # warm + result
+    k, rounds = 1, 0
+    while True:
+        t0 = time.perf_counter()
+        for _ in range(k):
+            O.hs512(host_u8, 0, n, w, threads=threads)
+        t = time.perf_counter() - t0
+        rounds += 1
+        if rounds >= 2 and t >= min_time:
+            break
+        k = k * 2 if 2 * t < min_time else max(k + 1, int(k * min_time / max(t, 1e-9) * 1.05) + 1)
+    return n * k / t / 1e9, threads, once, k, t
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (oracle port) on host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+    from oracle import oracle as O
+    cfg = args.config
+    kind, w, nbytes, desc = CONFIGS[cfg]
+    if cfg == "c4seg":
+        kind, w, nbytes = "bernoulli", 64, GIB
+    if kind == "uniform":
+        host = O.gen_uniform(nbytes, 0xC2 if cfg == "c2" else 0xC1)
+    elif kind == "onehot32":
+        host = O.gen_onehot32(nbytes, 0xC3)
+    elif kind == "bernoulli":
+        host = O.gen_bernoulli(nbytes, 0xC4, 655)
+    else:
+        host = O.gen_blocks(nbytes, 0xC5)
+    threads = host_threads()
+    for _ in range(args.warmup):
+        O.hs512(host, 0, host.size, w, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.hs512(host, 0, host.size, w, threads=threads)
+    t = time.perf_counter() - t0
+    value = host.size * args.steps / t / 1e9
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8" if w == 8 else f"u{w}",
+        "data": "synthetic (seeded splitmix64 generators, oracle/pospopcnt_oracle.c)",
+        "config": {"workload": desc, "word_width": w, "bytes_per_step": int(host.size)},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"whole {host.size >> 20} MiB {cfg} array per step; C "
+                                   "restatement of NumbaKernel.run (kernels.py:242-270) on "
+                                   f"{threads} threads over contiguous shards"},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------ GPU arm
+
+def main_gpu(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2412_16370_b200 as pp
+    from paper_2412_16370_b200 import _lib, gen
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.load()
+    st = torch.cuda.current_stream(dev)
+    sp = st.cuda_stream
+
+    cfg = args.config
+    kind, w, nbytes, desc = CONFIGS[cfg]
+    if args.width and cfg in ("c2",):
+        w = args.width
+    seed = {"c1": 0xC1, "c2": 0xC2, "c3": 0xC3, "c4": 0xC4, "c4seg": 0xC4 + 1, "c5": 0xC5}[cfg]
+    offset = 3 if cfg == "c4" else 0
+    alloc = nbytes + (64 if cfg == "c4" else 0)
+    word_unit = 4 if kind == "onehot32" else 8
+    buf = gen.generate(kind, alloc, seed, device=dev,
+                       word_offset=rank * alloc // word_unit, q=655)
+    view_ptr = buf.data_ptr() + offset
+    torch.cuda.synchronize()
+
+    counters = torch.zeros(64, dtype=torch.int64, device=dev)
+    glob = torch.zeros(64, dtype=torch.int64, device=dev)
+    seg_out = None
+    if cfg == "c4seg":
+        seg = 4096
+        nseg = nbytes // seg
+        seg_out = torch.zeros((nseg, w), dtype=torch.int64, device=dev)
+
+    def step():
+        if seg_out is not None:
+            _lib.check(lib.pp_count_fixed(view_ptr, 4096, nbytes // 4096, w, seg_out.data_ptr(),
+                                          _lib.PP_SEG_OVERWRITE, sp))
+        else:
+            _lib.check(lib.pp_count(view_ptr, nbytes, w, counters.data_ptr(), sp))
+        if world > 1:
+            glob.copy_(counters)
+            dist.all_reduce(glob)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        time.sleep(0.25 if args.steps >= 10 else 0.0)
+        e0.record(st)
+        for i in range(args.steps):
+            ev[i][0].record(st)
+            if seg_out is not None:
+                _lib.check(lib.pp_count_fixed(view_ptr, 4096, nbytes // 4096, w,
+                                              seg_out.data_ptr(), _lib.PP_SEG_OVERWRITE, sp))
+            else:
+                _lib.check(lib.pp_count(view_ptr, nbytes, w, counters.data_ptr(), sp))
+            ev[i][1].record(st)
+            if world > 1:
+                glob.copy_(counters)
+                dist.all_reduce(glob)
+        e1.record(st)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_ms = e0.elapsed_time(e1)
+    k_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    if world > 1:
+        tt = torch.tensor([t_ms, k_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms, k_ms = tt.tolist()
+    per_step_bytes = nbytes
+    value = world * per_step_bytes * args.steps / (t_ms / 1e3) / 1e9
+
+    # exactness vs the oracle (full array, C2 and C1 and c4)
+    exact = None
+    if args.check and cfg in ("c1", "c2", "c3", "c4", "c5") and rank == 0:
+        from oracle import oracle as O
+        host = buf.cpu().numpy()
+        want = O.hs512(host, offset, nbytes, w, threads=host_threads())
+        got = counters.cpu().numpy().view(np.uint64)[:w]
+        total = args.warmup + args.steps
+        exact = bool(all(int(g) == total * x for g, x in zip(got, want)))
+        del host
+
+    # the paper's read-only "roofline" kernel over the same bytes
+    sink = torch.zeros(1, dtype=torch.int64, device=dev)
+    for _ in range(max(3, args.warmup)):
+        _lib.check(lib.pp_readonly_sum(view_ptr, nbytes, sink.data_ptr(), sp))
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nro = max(5, args.steps)
+    r0.record(st)
+    for _ in range(nro):
+        _lib.check(lib.pp_readonly_sum(view_ptr, nbytes, sink.data_ptr(), sp))
+    r1.record(st)
+    torch.cuda.synchronize()
+    ro_gbs = nbytes * nro / (r0.elapsed_time(r1) / 1e3) / 1e9
+
+    peak, peak_src = load_peaks()
+    achieved = per_step_bytes / (k_ms / 1e3) / 1e9
+    kernel_key = "pp_seg_kernel" if seg_out is not None else "pp_tma_kernel<true>"
+    traffic = load_traffic(kernel_key)
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": kernel_key, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": per_step_bytes,
+                "readonly_roofline_gbs": round(ro_gbs, 1)}
+    if seg_out is not None:
+        seg_bytes_out = (nbytes // 4096) * w * 8
+        roofline["algorithmic_bytes_per_launch"] = per_step_bytes + seg_bytes_out
+        roofline["achieved"] = round((per_step_bytes + seg_bytes_out) / (k_ms / 1e3) / 1e9, 1)
+        roofline["frac"] = round(roofline["achieved"] / peak, 4)
+
+    # e2e through the public API from pinned host memory
+    e2e = None
+    if args.e2e and seg_out is None:
+        pinned = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        pinned.copy_(buf[offset:offset + nbytes])
+        torch.cuda.synchronize()
+        nst = max(2, min(args.steps, 5))
+        for _ in range(1):
+            pp.pospopcnt(pinned, w)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(nst):
+            res = pp.pospopcnt(pinned, w)  # H2D inside, D2H of the w counters
+        t_e2e = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = tt.item()
+        e2e = {"value": round(world * nbytes * nst / t_e2e / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": w * 8,
+               "path": "pospopcnt(pinned host tensor) -> pp_count_host: 32 MiB chunks, "
+                       "H2D on a copy stream overlapped with counting",
+               "steps": nst}
+        del pinned, res
+
+    cpu = None
+    if args.cpu_baseline and world == 1 and rank == 0 and seg_out is None:
+        sample = min(nbytes, 256 * MIB)
+        host = buf[offset:offset + sample].cpu().numpy()
+        gbs, threads, _, k, t = time_cpu_port(host, w, args.cpu_min_time)
+        cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+               "sample": f"first {sample >> 20} MiB of the same {cfg} array, counted {k}x "
+                         f"in {t:.1f} s (last of >=2 rounds); C restatement of "
+                         "NumbaKernel.run (kernels.py:242-270), contiguous shards on "
+                         f"{threads} host threads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(t_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8" if w == 8 else f"u{w}",
+            "data": "synthetic: seeded splitmix64 generators, generated in place in HBM",
+            "config": {"workload": desc, "word_width": w,
+                       "bytes_per_gpu_per_step": per_step_bytes,
+                       "parallelism": f"dp{world} (contiguous shards, NCCL allreduce of "
+                                      f"{w} counters per step)" if world > 1 else "single GPU",
+                       "l2": "input >> 126 MB L2, no flush needed" if nbytes > 256 * MIB
+                             else "input fits L2 (reported, not judged vs HBM)"},
+            "hbm_frac": round(value / world / peak, 4),
+            "words_per_s": round(value * 1e9 / (w // 8)),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+            "exact": exact,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--config", choices=tuple(CONFIGS), default="c2")
+    ap.add_argument("--width", type=int, default=0, help="override w for c2 (sweep)")
+    ap.add_argument("--no-check", dest="check", action="store_false")
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--cpu-min-time", type=float, default=5.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return main_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,136 @@
+/*
+ * pospopcnt_b200.h — C ABI of the B200 (sm_100a) positional population count.
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (/root/reference/pkg, pure Python) exposes the operation as a duck-typed
+ * kernel object whose `run(view, w, counters)` mutates a list of w counters
+ * (pkg/src/pospopcnt/kernels.py:242-270, NumbaKernel.run) behind the entry
+ * point `pospopcnt(data, width, counters=None, kernel=None)`
+ * (kernels.py:315-333).  The reference has no FFI of its own; the binding a
+ * maintainer adds is a ctypes kernel object over these symbols (see
+ * INTEGRATION.md).  Every entry point below replaces one reference interface,
+ * cited per function.
+ *
+ * Conventions
+ *  - plain C types only: pointers, sizes, ints; no torch/CUDA C++ types.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *  - device entry points are asynchronous on `stream`; they never synchronise
+ *    except where stated.
+ *  - counters are 64-bit unsigned integers, one per bit position, and are
+ *    ACCUMULATED into, never cleared (core.py:82-87).
+ *  - return 0 on success, otherwise a PP_E* code; pp_last_error() gives a
+ *    thread-local message for the last failure on the calling thread.
+ *  - word assembly is little-endian, bit position 0 = least significant bit
+ *    of a word (core.py:3-6).
+ *  - results do not depend on the alignment of `data` nor on bytes outside
+ *    [data, data+nbytes) (pkg/tests/test_kernels.py:75-91); no byte outside
+ *    that range is ever read.
+ */
+#ifndef POSPOPCNT_B200_H
+#define POSPOPCNT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PP_API __attribute__((visibility("default")))
+#else
+#define PP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PP_ABI_VERSION 1
+
+/* error codes (mirroring the reference's exception classes, core.py:19-34) */
+#define PP_OK        0
+#define PP_EWIDTH    1  /* width not in {8,16,32,64}      -> ValueError (core.py:31-34)       */
+#define PP_ELENGTH   2  /* nbytes not word-complete        -> InputLengthError (core.py:68-74) */
+#define PP_ECUDA     3  /* CUDA runtime error              -> RuntimeError                     */
+#define PP_EARG      4  /* bad pointer / argument          -> ValueError                       */
+#define PP_ENODEV    5  /* no usable sm_100 device         -> KernelUnavailableError           */
+
+/* flags for the segmented entry points */
+#define PP_SEG_ACCUMULATE 0  /* out[s*w+j] += count (reference semantics)  */
+#define PP_SEG_OVERWRITE  1  /* out[s*w+j]  = count (fresh counter rows)   */
+
+PP_API int         pp_abi_version(void);
+PP_API const char *pp_strerror(int code);
+PP_API const char *pp_last_error(void);
+
+/* Number of SMs / sm major.minor of `device`; used for launch sizing. */
+PP_API int pp_device_info(int device, int *num_sms, int *cc_major, int *cc_minor);
+
+/*
+ * pp_count — counters[j] += #{words k : bit j of word k is set}, j < width.
+ *
+ * data:     DEVICE pointer to nbytes bytes (any alignment).
+ * counters: DEVICE pointer to `width` uint64 counters (8-byte aligned).
+ * Replaces: NumbaKernel.run / Kernel.run(view, w, counters)
+ *           (kernels.py:242-270; protocol kernels.py:93, 178, 242) and the
+ *           dispatch body of pospopcnt() (kernels.py:315-333).
+ * Errors:   PP_EWIDTH (check_width, core.py:31-34), PP_ELENGTH
+ *           (InputView.check_complete, core.py:68-74), PP_EARG (host pointer).
+ */
+PP_API int pp_count(const void *data, size_t nbytes, int width,
+             unsigned long long *counters, void *stream);
+
+/*
+ * pp_count_host — the same count over a HOST buffer (pinned or pageable):
+ * pipelined host->device copies overlapped with counting, result added into
+ * HOST counters.  Synchronous.  Replaces the bytes-like path of pospopcnt()
+ * (kernels.py:315-333 with data = bytes/bytearray/memoryview; cli.py:82-94).
+ */
+PP_API int pp_count_host(const void *host_data, size_t nbytes, int width,
+                  unsigned long long *host_counters);
+
+/*
+ * pp_count_segmented — many independent arrays in one launch.
+ * Segment s is device bytes [base + seg_off[s], base + seg_off[s+1]);
+ * out (DEVICE, nseg*width uint64, row-major) row s receives its counters.
+ * seg_off is a DEVICE array of nseg+1 non-decreasing byte offsets; every
+ * segment length must be a multiple of width/8 (caller-validated).
+ * Replaces: nseg calls of Kernel.run (kernels.py:242) each with its own
+ * counter list; the reference's short-array path is edges.py:96-102.
+ */
+PP_API int pp_count_segmented(const void *base, const unsigned long long *seg_off,
+                       size_t nseg, int width, unsigned long long *out,
+                       int flags, void *stream);
+
+/* pp_count_fixed — as above for nseg equal segments of seg_bytes each. */
+PP_API int pp_count_fixed(const void *base, size_t seg_bytes, size_t nseg, int width,
+                   unsigned long long *out, int flags, void *stream);
+
+/*
+ * pp_readonly_sum — the paper's "roofline" dummy kernel:
+ * streams nbytes through exactly the load path of pp_count and XORs them into
+ * *sink (DEVICE, 1 uint64).  Measurement only.
+ */
+PP_API int pp_readonly_sum(const void *data, size_t nbytes, unsigned long long *sink,
+                    void *stream);
+
+/* ---- seeded synthetic inputs, generated in place on the device ----------
+ * Benchmark/test infrastructure.  Byte-identical twins
+ * live in oracle/pospopcnt_oracle.c.  word_offset lets a shard generate its
+ * slice of a larger logical array.  dst must be 8-byte aligned.           */
+
+/* uniform bits: u64 word g = splitmix64(seed + (g+1)*golden) */
+PP_API int pp_gen_uniform(void *dst, size_t nbytes, uint64_t seed, uint64_t word_offset,
+                   void *stream);
+/* Bernoulli(q/65536) bits, q in [0, 65536], via a 16-draw AND/OR ladder */
+PP_API int pp_gen_bernoulli(void *dst, size_t nbytes, uint64_t seed, uint64_t word_offset,
+                     uint32_t q, void *stream);
+/* per-block Bernoulli: block b (block_bytes each) has q_b = mix(seed', b) mod 65537 */
+PP_API int pp_gen_blocks(void *dst, size_t nbytes, uint64_t seed, uint64_t word_offset,
+                  uint64_t block_bytes, void *stream);
+/* one-hot u32 words: bit = #{k < 31 : thresholds[k] <= u}, u uniform u32 */
+PP_API int pp_gen_onehot32(void *dst, size_t nbytes, uint64_t seed, uint64_t word_offset,
+                    const uint32_t *thresholds31, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* POSPOPCNT_B200_H */

@@ -1,0 +1,92 @@
+"""ctypes binding of libpospopcnt_b200.so (include/pospopcnt_b200.h).
+
+The library is built in-tree by ``paper_2412_16370_b200.build``.  If it is
+missing or cannot be loaded, every entry point raises KernelUnavailableError:
+there is no CPU fallback anywhere in this package.  ctypes releases the GIL
+for the duration of each call.
+"""
+
+import ctypes
+import os
+import threading
+
+from .core import InputLengthError, KernelUnavailableError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpospopcnt_b200.so")
+
+PP_OK, PP_EWIDTH, PP_ELENGTH, PP_ECUDA, PP_EARG, PP_ENODEV = range(6)
+PP_SEG_ACCUMULATE, PP_SEG_OVERWRITE = 0, 1
+ABI_VERSION = 1
+
+# name -> (restype, argtypes); mirrors include/pospopcnt_b200.h
+_vp, _sz, _int, _u64, _u32 = (ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
+                               ctypes.c_uint64, ctypes.c_uint32)
+SIGNATURES = {
+    "pp_abi_version": (_int, []),
+    "pp_strerror": (ctypes.c_char_p, [_int]),
+    "pp_last_error": (ctypes.c_char_p, []),
+    "pp_device_info": (_int, [_int, _vp, _vp, _vp]),
+    "pp_count": (_int, [_vp, _sz, _int, _vp, _vp]),
+    "pp_count_host": (_int, [_vp, _sz, _int, _vp]),
+    "pp_count_segmented": (_int, [_vp, _vp, _sz, _int, _vp, _int, _vp]),
+    "pp_count_fixed": (_int, [_vp, _sz, _sz, _int, _vp, _int, _vp]),
+    "pp_readonly_sum": (_int, [_vp, _sz, _vp, _vp]),
+    "pp_gen_uniform": (_int, [_vp, _sz, _u64, _u64, _vp]),
+    "pp_gen_bernoulli": (_int, [_vp, _sz, _u64, _u64, _u32, _vp]),
+    "pp_gen_blocks": (_int, [_vp, _sz, _u64, _u64, _u64, _vp]),
+    "pp_gen_onehot32": (_int, [_vp, _sz, _u64, _u64, _vp, _vp]),
+}
+
+_lock = threading.Lock()
+_lib = None
+_load_error = None
+
+
+def load():
+    """Load (building first if absent) and type the shared library."""
+    global _lib, _load_error
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if _load_error is not None:
+            raise KernelUnavailableError(_load_error)
+        try:
+            if not os.path.exists(LIB_PATH):
+                from . import build as _build
+                _build.build()
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                f = getattr(lib, name)
+                f.restype = res
+                f.argtypes = args
+            if lib.pp_abi_version() != ABI_VERSION:
+                raise RuntimeError("ABI version mismatch")
+        except Exception as exc:  # noqa: BLE001 - reported loudly below
+            _load_error = f"libpospopcnt_b200.so unavailable: {exc}"
+            raise KernelUnavailableError(_load_error) from exc
+        _lib = lib
+        return _lib
+
+
+def check(rc):
+    """Map a PP_E* return code to the reference's exception classes."""
+    if rc == PP_OK:
+        return
+    msg = (_lib.pp_last_error() or b"").decode() or _lib.pp_strerror(rc).decode()
+    if rc == PP_ELENGTH:
+        raise InputLengthError(msg)
+    if rc in (PP_EWIDTH, PP_EARG):
+        raise ValueError(msg)
+    if rc == PP_ENODEV:
+        raise KernelUnavailableError(msg)
+    raise RuntimeError(msg)
+
+
+def device_info(device=0):
+    lib = load()
+    sms, ma, mi = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    check(lib.pp_device_info(device, ctypes.byref(sms), ctypes.byref(ma), ctypes.byref(mi)))
+    return {"num_sms": sms.value, "cc": (ma.value, mi.value)}

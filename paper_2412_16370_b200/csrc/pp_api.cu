@@ -1,0 +1,334 @@
+// pp_api.cu — the C ABI (include/pospopcnt_b200.h): validation, launch
+// sizing, error mapping and the pipelined host-buffer path.
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/pospopcnt_b200.h"
+#include "pp_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char *where) {
+  return fail(PP_ECUDA, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+bool width_ok(int w) { return w == 8 || w == 16 || w == 32 || w == 64; }
+
+// Which load path feeds the counting kernel.  TMA bulk copies are the
+// default; PP_LOAD_PATH=ldg selects the register-fed variant for A/B runs.
+pp::LoadPath load_path() {
+  static pp::LoadPath path = [] {
+    const char *s = std::getenv("PP_LOAD_PATH");
+    return (s && std::strcmp(s, "ldg") == 0) ? pp::LoadPath::kLdg : pp::LoadPath::kTma;
+  }();
+  return path;
+}
+
+int current_devinfo(pp::DevInfo *di) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  e = pp::device_info(dev, di);
+  if (e != cudaSuccess) return cuda_fail(e, "device_info");
+  if (di->cc_major != 10)
+    return fail(PP_ENODEV, "device %d is sm_%d%d; this build targets sm_100a", dev,
+                di->cc_major, di->cc_minor);
+  return PP_OK;
+}
+
+// Device memory (or managed) check; a host pointer handed to a kernel would
+// fault the GPU, so it is rejected here.
+int check_device_ptr(const void *p, const char *what) {
+  if (!p) return fail(PP_EARG, "%s is NULL", what);
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(PP_EARG, "%s: not a CUDA pointer (%s)", what, cudaGetErrorString(e));
+  }
+  if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+    return fail(PP_EARG, "%s must be device memory", what);
+  return PP_OK;
+}
+
+int count_device(const void *data, size_t nbytes, int width, unsigned long long *counters,
+                 cudaStream_t st, const pp::DevInfo &di) {
+  pp::CountArgs a{};
+  const pp::LoadPath path = load_path();
+  pp::split_range(static_cast<const uint8_t *>(data), nbytes, pp::count_chunk_bytes(path), &a);
+  a.counters = counters;
+  a.width = width;
+  cudaError_t e = pp::launch_count(a, path, di, st);
+  if (e != cudaSuccess) return cuda_fail(e, "pp_count launch");
+  return PP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pp_abi_version(void) { return PP_ABI_VERSION; }
+
+const char *pp_strerror(int code) {
+  switch (code) {
+    case PP_OK: return "ok";
+    case PP_EWIDTH: return "word width must be one of (8, 16, 32, 64)";
+    case PP_ELENGTH: return "input length is not a multiple of the word size";
+    case PP_ECUDA: return "CUDA error";
+    case PP_EARG: return "invalid argument";
+    case PP_ENODEV: return "no usable sm_100 device";
+    default: return "unknown error";
+  }
+}
+
+const char *pp_last_error(void) { return g_err.c_str(); }
+
+int pp_device_info(int device, int *num_sms, int *cc_major, int *cc_minor) {
+  pp::DevInfo di;
+  cudaError_t e = pp::device_info(device, &di);
+  if (e != cudaSuccess) return cuda_fail(e, "pp_device_info");
+  if (num_sms) *num_sms = di.num_sms;
+  if (cc_major) *cc_major = di.cc_major;
+  if (cc_minor) *cc_minor = di.cc_minor;
+  return PP_OK;
+}
+
+int pp_count(const void *data, size_t nbytes, int width, unsigned long long *counters,
+             void *stream) {
+  if (!width_ok(width)) return fail(PP_EWIDTH, "word width must be one of (8, 16, 32, 64), got %d", width);
+  if (nbytes % (size_t)(width / 8))
+    return fail(PP_ELENGTH, "%zu bytes is not a multiple of the %d-byte word size", nbytes,
+                width / 8);
+  int rc;
+  if ((rc = check_device_ptr(counters, "counters"))) return rc;
+  if (nbytes == 0) return PP_OK;  // counters unchanged (core.py:82-96 on empty input)
+  if ((rc = check_device_ptr(data, "data"))) return rc;
+  pp::DevInfo di;
+  if ((rc = current_devinfo(&di))) return rc;
+  return count_device(data, nbytes, width, counters, static_cast<cudaStream_t>(stream), di);
+}
+
+static int seg_common(const pp::SegArgs &a, void *stream) {
+  if (!width_ok(a.width)) return fail(PP_EWIDTH, "word width must be one of (8, 16, 32, 64), got %d", a.width);
+  if (a.nseg == 0) return PP_OK;
+  int rc;
+  if ((rc = check_device_ptr(a.out, "out"))) return rc;
+  if ((rc = check_device_ptr(a.base, "base"))) return rc;
+  if (a.seg_off && (rc = check_device_ptr(a.seg_off, "seg_off"))) return rc;
+  pp::DevInfo di;
+  if ((rc = current_devinfo(&di))) return rc;
+  cudaError_t e = pp::launch_segmented(a, di, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "pp_count_segmented launch");
+  return PP_OK;
+}
+
+int pp_count_segmented(const void *base, const unsigned long long *seg_off, size_t nseg,
+                       int width, unsigned long long *out, int flags, void *stream) {
+  if (!seg_off && nseg) return fail(PP_EARG, "seg_off is NULL");
+  pp::SegArgs a{};
+  a.base = static_cast<const uint8_t *>(base);
+  a.seg_off = seg_off;
+  a.nseg = nseg;
+  a.out = out;
+  a.width = width;
+  a.overwrite = (flags & PP_SEG_OVERWRITE) ? 1 : 0;
+  return seg_common(a, stream);
+}
+
+int pp_count_fixed(const void *base, size_t seg_bytes, size_t nseg, int width,
+                   unsigned long long *out, int flags, void *stream) {
+  if (width_ok(width) && seg_bytes % (size_t)(width / 8))
+    return fail(PP_ELENGTH, "%zu bytes is not a multiple of the %d-byte word size", seg_bytes,
+                width / 8);
+  pp::SegArgs a{};
+  a.base = static_cast<const uint8_t *>(base);
+  a.seg_off = nullptr;
+  a.seg_bytes = seg_bytes;
+  a.nseg = nseg;
+  a.out = out;
+  a.width = width;
+  a.overwrite = (flags & PP_SEG_OVERWRITE) ? 1 : 0;
+  return seg_common(a, stream);
+}
+
+int pp_readonly_sum(const void *data, size_t nbytes, unsigned long long *sink, void *stream) {
+  int rc;
+  if ((rc = check_device_ptr(sink, "sink"))) return rc;
+  if (nbytes == 0) return PP_OK;
+  if ((rc = check_device_ptr(data, "data"))) return rc;
+  pp::DevInfo di;
+  if ((rc = current_devinfo(&di))) return rc;
+  pp::CountArgs a{};
+  pp::split_range(static_cast<const uint8_t *>(data), nbytes,
+                  pp::count_chunk_bytes(pp::LoadPath::kTma), &a);
+  cudaError_t e = pp::launch_readonly(a, sink, di, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "pp_readonly_sum launch");
+  return PP_OK;
+}
+
+// ---------------------------------------------------------------- host path
+// Per-thread staging context: NBUF device buffers, a copy stream and a count
+// stream.  Chunk i is copied H2D into buffer i % NBUF on the copy stream while
+// chunk i-1 is counted on the count stream; the chunks are word-complete
+// (CHUNK is a multiple of 64), so their counts simply add.
+namespace {
+constexpr int kNbuf = 3;
+constexpr size_t kChunk = 32ull << 20;
+
+struct HostCtx {
+  int dev = -1;
+  cudaStream_t copy = nullptr, count = nullptr;
+  void *buf[kNbuf] = {};
+  cudaEvent_t copied[kNbuf] = {}, freed[kNbuf] = {};
+  unsigned long long *dcnt = nullptr;
+  unsigned long long *hcnt = nullptr;  // pinned
+  // no destructor: the context lives until process exit (tearing CUDA
+  // objects down from thread_local destructors races the runtime's own exit).
+  void release() {
+    if (dev < 0) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(dev);
+    for (int i = 0; i < kNbuf; ++i) {
+      if (buf[i]) cudaFree(buf[i]);
+      if (copied[i]) cudaEventDestroy(copied[i]);
+      if (freed[i]) cudaEventDestroy(freed[i]);
+      buf[i] = nullptr;
+      copied[i] = freed[i] = nullptr;
+    }
+    if (dcnt) cudaFree(dcnt);
+    if (hcnt) cudaFreeHost(hcnt);
+    if (copy) cudaStreamDestroy(copy);
+    if (count) cudaStreamDestroy(count);
+    dcnt = nullptr;
+    hcnt = nullptr;
+    copy = count = nullptr;
+    dev = -1;
+    cudaSetDevice(cur);
+  }
+  cudaError_t ensure(int d) {
+    if (dev == d) return cudaSuccess;
+    release();
+    cudaError_t e;
+    dev = d;
+    if ((e = cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking))) return e;
+    if ((e = cudaStreamCreateWithFlags(&count, cudaStreamNonBlocking))) return e;
+    for (int i = 0; i < kNbuf; ++i) {
+      if ((e = cudaMalloc(&buf[i], kChunk))) return e;
+      if ((e = cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming))) return e;
+      if ((e = cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming))) return e;
+    }
+    if ((e = cudaMalloc(&dcnt, 64 * sizeof(unsigned long long)))) return e;
+    if ((e = cudaMallocHost(&hcnt, 64 * sizeof(unsigned long long)))) return e;
+    return cudaSuccess;
+  }
+};
+thread_local HostCtx g_host;
+}  // namespace
+
+int pp_count_host(const void *host_data, size_t nbytes, int width,
+                  unsigned long long *host_counters) {
+  if (!width_ok(width)) return fail(PP_EWIDTH, "word width must be one of (8, 16, 32, 64), got %d", width);
+  if (nbytes % (size_t)(width / 8))
+    return fail(PP_ELENGTH, "%zu bytes is not a multiple of the %d-byte word size", nbytes,
+                width / 8);
+  if (!host_counters) return fail(PP_EARG, "host_counters is NULL");
+  if (nbytes == 0) return PP_OK;
+  if (!host_data) return fail(PP_EARG, "host_data is NULL");
+  int rc;
+  pp::DevInfo di;
+  if ((rc = current_devinfo(&di))) return rc;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaError_t e = g_host.ensure(dev);
+  if (e != cudaSuccess) return cuda_fail(e, "pp_count_host setup");
+  HostCtx &h = g_host;
+  if ((e = cudaMemsetAsync(h.dcnt, 0, 64 * sizeof(unsigned long long), h.count)))
+    return cuda_fail(e, "cudaMemsetAsync");
+  const uint8_t *src = static_cast<const uint8_t *>(host_data);
+  size_t off = 0;
+  for (size_t i = 0; off < nbytes; ++i) {
+    const int b = (int)(i % kNbuf);
+    const size_t len = (nbytes - off) < kChunk ? (nbytes - off) : kChunk;
+    if ((e = cudaStreamWaitEvent(h.copy, h.freed[b], 0))) return cuda_fail(e, "wait freed");
+    if ((e = cudaMemcpyAsync(h.buf[b], src + off, len, cudaMemcpyHostToDevice, h.copy)))
+      return cuda_fail(e, "cudaMemcpyAsync H2D");
+    if ((e = cudaEventRecord(h.copied[b], h.copy))) return cuda_fail(e, "record copied");
+    if ((e = cudaStreamWaitEvent(h.count, h.copied[b], 0))) return cuda_fail(e, "wait copied");
+    if ((rc = count_device(h.buf[b], len, width, h.dcnt, h.count, di))) return rc;
+    if ((e = cudaEventRecord(h.freed[b], h.count))) return cuda_fail(e, "record freed");
+    off += len;
+  }
+  if ((e = cudaMemcpyAsync(h.hcnt, h.dcnt, (size_t)width * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, h.count)))
+    return cuda_fail(e, "cudaMemcpyAsync D2H");
+  if ((e = cudaStreamSynchronize(h.count))) return cuda_fail(e, "cudaStreamSynchronize");
+  for (int j = 0; j < width; ++j) host_counters[j] += h.hcnt[j];
+  return PP_OK;
+}
+
+// ------------------------------------------------------------ generators
+static int gen_check(void *dst, size_t nbytes, size_t unit) {
+  if (nbytes % unit) return fail(PP_ELENGTH, "generator length %zu not a multiple of %zu", nbytes, unit);
+  if (nbytes == 0) return PP_OK;
+  if (((uintptr_t)dst) % unit) return fail(PP_EARG, "generator dst must be %zu-byte aligned", unit);
+  return check_device_ptr(dst, "dst");
+}
+
+int pp_gen_uniform(void *dst, size_t nbytes, uint64_t seed, uint64_t word_offset, void *stream) {
+  int rc;
+  if ((rc = gen_check(dst, nbytes, 8)) || !nbytes) return rc;
+  cudaError_t e = pp::launch_gen_uniform(static_cast<uint64_t *>(dst), nbytes / 8, seed,
+                                         word_offset, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? PP_OK : cuda_fail(e, "pp_gen_uniform");
+}
+
+int pp_gen_bernoulli(void *dst, size_t nbytes, uint64_t seed, uint64_t word_offset, uint32_t q,
+                     void *stream) {
+  int rc;
+  if (q > 65536u) return fail(PP_EARG, "q must be in [0, 65536]");
+  if ((rc = gen_check(dst, nbytes, 8)) || !nbytes) return rc;
+  cudaError_t e = pp::launch_gen_bernoulli(static_cast<uint64_t *>(dst), nbytes / 8, seed,
+                                           word_offset, q, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? PP_OK : cuda_fail(e, "pp_gen_bernoulli");
+}
+
+int pp_gen_blocks(void *dst, size_t nbytes, uint64_t seed, uint64_t word_offset,
+                  uint64_t block_bytes, void *stream) {
+  int rc;
+  if (block_bytes == 0 || block_bytes % 8) return fail(PP_EARG, "block_bytes must be a positive multiple of 8");
+  if ((rc = gen_check(dst, nbytes, 8)) || !nbytes) return rc;
+  cudaError_t e = pp::launch_gen_blocks(static_cast<uint64_t *>(dst), nbytes / 8, seed,
+                                        word_offset, block_bytes, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? PP_OK : cuda_fail(e, "pp_gen_blocks");
+}
+
+int pp_gen_onehot32(void *dst, size_t nbytes, uint64_t seed, uint64_t word_offset,
+                    const uint32_t *thresholds31, void *stream) {
+  int rc;
+  if (!thresholds31) return fail(PP_EARG, "thresholds31 is NULL");
+  if ((rc = gen_check(dst, nbytes, 4)) || !nbytes) return rc;
+  cudaError_t e = pp::launch_gen_onehot32(static_cast<uint32_t *>(dst), nbytes / 4, seed,
+                                          word_offset, thresholds31,
+                                          static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? PP_OK : cuda_fail(e, "pp_gen_onehot32");
+}
+
+}  // extern "C"

@@ -1,0 +1,350 @@
+// pp_count.cu — sm_100a kernels of the positional population count.
+//
+// Hot path (replaces NumbaKernel.run + _nbkern.run_main, kernels.py:242-270,
+// _nbkern.py:43-177):
+//
+//   pp_count_tma_kernel   persistent, one CTA per SM.  One elected producer
+//                         thread streams 32 KiB chunks of the aligned body
+//                         HBM -> shared memory with cp.async.bulk (UBLKCP),
+//                         NSTAGE-deep mbarrier ring; 8 consumer warps read
+//                         the stage with conflict-free LDS.128 and run the
+//                         two-level carry-save count (pp_device.cuh).
+//   pp_count_ldg_kernel   same arithmetic fed by LDG.128 straight to
+//                         registers (tuning alternative / A-B evidence).
+//
+// Both finish with a warp bit-transpose + __popc per bit position, a shared
+// u64 frame[64] per CTA, and one u64 atomicAdd per (CTA, counter) after the
+// rotate-and-fold of flush_fw (accumulate.py:115-130).
+//
+// Segmented mode: pp_seg_kernel, one warp per segment.
+#include "pp_device.cuh"
+#include "pp_internal.h"
+
+namespace pp {
+
+constexpr int kTmaConsumerWarps = 8;
+constexpr int kTmaStages = 6;
+constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
+constexpr int kTmaStageVecs = kTmaConsumerWarps * 32 * 8;  // 2048 x 16 B = 32 KiB
+constexpr unsigned long long kTmaStageBytes = kTmaStageVecs * 16ull;
+constexpr size_t kTmaSmemBytes = kTmaStages * kTmaStageBytes + 2 * kTmaStages * 8;
+
+constexpr int kLdgWarps = 8;
+constexpr int kLdgThreads = kLdgWarps * 32;
+constexpr int kLdgChunkVecs = kLdgThreads * 8;
+constexpr unsigned long long kLdgChunkBytes = kLdgChunkVecs * 16ull;
+
+constexpr int kSegThreads = 256;
+
+// Head/tail bytes (< 16 each) as one extra weight-1 plane pair, counted by
+// warp 0 of CTA 0.  Lane l < 16 takes head byte l, lane 16+l tail byte l.
+__device__ __forceinline__ void count_edges(Counter &c, const uint8_t *head, uint32_t hb,
+                                            const uint8_t *tail, uint32_t tb, uint32_t lane,
+                                            const TC &t) {
+  const uint8_t *p = nullptr;
+  if (lane < 16) {
+    if (lane < hb) p = head + lane;
+  } else if (lane - 16 < tb) {
+    p = tail + (lane - 16);
+  }
+  unsigned long long fw = 0;
+  if (p) fw = (unsigned long long)__ldg(p) << frame_shift(p);
+  c.ce += wcount((uint32_t)fw, t);
+  c.co += wcount((uint32_t)(fw >> 32), t);
+}
+
+// counters[j] += sum_{i = j mod w} frame[(i + rot) mod 64]   (flush_fw)
+__device__ __forceinline__ void fold_frame_to_counters(const unsigned long long *frame,
+                                                       unsigned long long *counters,
+                                                       int width, int rot) {
+  int j = threadIdx.x;
+  if (j < width) {
+    unsigned long long s = 0;
+    for (int i = j; i < 64; i += width) s += frame[(i + rot) & 63];
+    if (s) atomicAdd(counters + j, s);
+  }
+}
+
+template <bool kCount>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    pp_tma_kernel(CountArgs a, unsigned long long *sink) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint4 *stages = reinterpret_cast<uint4 *>(smem);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kTmaStages * kTmaStageBytes);
+  uint64_t *empty = full + kTmaStages;
+  __shared__ unsigned long long frame[64];
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTmaConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  if (threadIdx.x < 64) frame[threadIdx.x] = 0;
+  __syncthreads();
+
+  const unsigned long long nchunks = a.nchunks;
+  if (warp == kTmaConsumerWarps) {
+    // ---------------- producer: one elected thread issues bulk copies
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      uint32_t stage = 0, phase = 0;
+      for (unsigned long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        const unsigned long long off = ch * kTmaStageBytes;
+        const unsigned long long rem = a.body_bytes - off;
+        const uint32_t bytes = (uint32_t)(rem < kTmaStageBytes ? rem : kTmaStageBytes);
+        mbar_arrive_expect_tx(&full[stage], bytes);
+        bulk_g2s(stages + stage * kTmaStageVecs, a.body + off, bytes, &full[stage], pol);
+        if (++stage == kTmaStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---------------- consumers
+    const TC t = make_tc(lane);
+    Counter c;
+    c.init();
+    uint32_t xs = 0;  // read-only roofline accumulator
+    uint32_t stage = 0, phase = 0;
+    const uint32_t tid = threadIdx.x;
+    for (unsigned long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+      mbar_wait(&full[stage], phase);
+      const uint4 *sv = stages + stage * kTmaStageVecs;
+      uint4 v[8];
+      const unsigned long long off = ch * kTmaStageBytes;
+      const unsigned long long rem = a.body_bytes - off;
+      if (rem >= kTmaStageBytes) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = sv[tid + i * (kTmaConsumerWarps * 32)];
+      } else {
+        const uint32_t nv = (uint32_t)(rem >> 4);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t idx = tid + i * (kTmaConsumerWarps * 32);
+          v[i] = idx < nv ? sv[idx] : make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (kCount) {
+        c.eat8(v, t);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) xs ^= v[i].x ^ v[i].y ^ v[i].z ^ v[i].w;
+      }
+      if (++stage == kTmaStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    if (kCount) {
+      c.finish(t);
+      if (blockIdx.x == 0 && warp == 0)
+        count_edges(c, a.head, a.head_bytes, a.tail, a.tail_bytes, lane, t);
+      atomicAdd(&frame[lane], c.ce);
+      atomicAdd(&frame[32 + lane], c.co);
+    } else {
+      xs = __reduce_xor_sync(FULL, xs);
+      if (lane == 0) atomicXor(sink, (unsigned long long)xs);
+    }
+  }
+  __syncthreads();
+  if (kCount) fold_frame_to_counters(frame, a.counters, a.width, a.rot);
+}
+
+__global__ void __launch_bounds__(kLdgThreads)
+    pp_count_ldg_kernel(CountArgs a) {
+  __shared__ unsigned long long frame[64];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < 64) frame[threadIdx.x] = 0;
+  __syncthreads();
+  const TC t = make_tc(lane);
+  Counter c;
+  c.init();
+  const uint4 *body = reinterpret_cast<const uint4 *>(a.body);
+  const unsigned long long nvec = a.body_bytes >> 4;
+  for (unsigned long long ch = blockIdx.x; ch < a.nchunks; ch += gridDim.x) {
+    const unsigned long long base = ch * kLdgChunkVecs + threadIdx.x;
+    uint4 v[8];
+    if ((ch + 1) * kLdgChunkVecs <= nvec) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = ldg_stream(body + base + i * kLdgThreads);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const unsigned long long idx = base + i * kLdgThreads;
+        v[i] = idx < nvec ? ldg_stream(body + idx) : make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    c.eat8(v, t);
+  }
+  c.finish(t);
+  if (blockIdx.x == 0 && warp == 0)
+    count_edges(c, a.head, a.head_bytes, a.tail, a.tail_bytes, lane, t);
+  atomicAdd(&frame[lane], c.ce);
+  atomicAdd(&frame[32 + lane], c.co);
+  __syncthreads();
+  fold_frame_to_counters(frame, a.counters, a.width, a.rot);
+}
+
+// One warp per segment; grid-stride over segments.  Each lane eats groups of
+// 8 coalesced 16-byte vectors; the segment's <16-byte head and tail become
+// one extra weight-1 plane.  Row s of out gets the rotated/folded counts.
+__global__ void __launch_bounds__(kSegThreads)
+    pp_seg_kernel(SegArgs a) {
+  const uint32_t lane = threadIdx.x & 31;
+  const unsigned long long gw = (blockIdx.x * (unsigned long long)kSegThreads + threadIdx.x) >> 5;
+  const unsigned long long nw = (gridDim.x * (unsigned long long)kSegThreads) >> 5;
+  const TC t = make_tc(lane);
+  const int w = a.width;
+  for (unsigned long long s = gw; s < a.nseg; s += nw) {
+    unsigned long long s0, s1;
+    if (a.seg_off) {
+      s0 = a.seg_off[s];
+      s1 = a.seg_off[s + 1];
+      if (s1 < s0) s1 = s0;
+    } else {
+      s0 = s * a.seg_bytes;
+      s1 = s0 + a.seg_bytes;
+    }
+    const uint8_t *p0 = a.base + s0;
+    const unsigned long long n = s1 - s0;
+    const unsigned long long mis = (16u - ((uintptr_t)p0 & 15u)) & 15u;
+    const unsigned long long hb = mis < n ? mis : n;
+    const unsigned long long nv = (n - hb) >> 4;
+    const uint4 *body = reinterpret_cast<const uint4 *>(p0 + hb);
+    const uint32_t tb = (uint32_t)(n - hb - (nv << 4));
+    Counter c;
+    c.init();
+    for (unsigned long long g = 0; g < nv; g += 256) {
+      uint4 v[8];
+      if (g + 256 <= nv) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = ldg_stream(body + g + j * 32 + lane);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const unsigned long long idx = g + j * 32 + lane;
+          v[j] = idx < nv ? ldg_stream(body + idx) : make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
+      c.eat8(v, t);
+    }
+    if (hb | tb) count_edges(c, p0, (uint32_t)hb, (const uint8_t *)(body + nv), tb, lane, t);
+    c.finish(t);
+    const int rot = (int)frame_shift(p0);
+    unsigned long long *row = a.out + s * (unsigned long long)w;
+    if (w == 64) {
+      const int j0 = ((int)lane - rot) & 63, j1 = ((int)lane + 32 - rot) & 63;
+      if (a.overwrite) {
+        row[j0] = c.ce;
+        row[j1] = c.co;
+      } else {
+        row[j0] += c.ce;
+        row[j1] += c.co;
+      }
+    } else {
+      unsigned long long tot = c.ce + c.co;
+      if (w <= 16) tot += __shfl_xor_sync(FULL, tot, 16);
+      if (w <= 8) tot += __shfl_xor_sync(FULL, tot, 8);
+      if ((int)lane < w) {
+        const int j = ((int)lane - rot) & (w - 1);
+        if (a.overwrite)
+          row[j] = tot;
+        else
+          row[j] += tot;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host side
+void split_range(const uint8_t *data, unsigned long long nbytes,
+                 unsigned long long chunk_bytes, CountArgs *a) {
+  const unsigned long long mis = (16u - ((uintptr_t)data & 15u)) & 15u;
+  const unsigned long long hb = mis < nbytes ? mis : nbytes;
+  const unsigned long long body = (nbytes - hb) & ~15ull;
+  a->head = data;
+  a->head_bytes = (uint32_t)hb;
+  a->body = data + hb;
+  a->body_bytes = body;
+  a->nchunks = (body + chunk_bytes - 1) / chunk_bytes;
+  a->tail = data + hb + body;
+  a->tail_bytes = (uint32_t)(nbytes - hb - body);
+  a->rot = (int)(8u * ((uintptr_t)data & 7u));
+}
+
+unsigned long long count_chunk_bytes(LoadPath path) {
+  return path == LoadPath::kTma ? kTmaStageBytes : kLdgChunkBytes;
+}
+
+cudaError_t device_info(int dev, DevInfo *out) {
+  static DevInfo cache[64];
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!cache[dev].ready) {
+    DevInfo d{};
+    cudaError_t e;
+    if ((e = cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev))) return e;
+    if ((e = cudaDeviceGetAttribute(&d.cc_major, cudaDevAttrComputeCapabilityMajor, dev))) return e;
+    if ((e = cudaDeviceGetAttribute(&d.cc_minor, cudaDevAttrComputeCapabilityMinor, dev))) return e;
+    if ((e = cudaFuncSetAttribute(pp_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kTmaSmemBytes)))
+      return e;
+    if ((e = cudaFuncSetAttribute(pp_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kTmaSmemBytes)))
+      return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.seg_blocks_per_sm, pp_seg_kernel,
+                                                           kSegThreads, 0)))
+      return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.ldg_blocks_per_sm,
+                                                           pp_count_ldg_kernel, kLdgThreads, 0)))
+      return e;
+    if (d.seg_blocks_per_sm < 1) d.seg_blocks_per_sm = 1;
+    if (d.ldg_blocks_per_sm < 1) d.ldg_blocks_per_sm = 1;
+    d.ready = true;
+    cache[dev] = d;
+  }
+  *out = cache[dev];
+  return cudaSuccess;
+}
+
+static unsigned grid_for(unsigned long long nchunks, unsigned long long cap) {
+  unsigned long long g = nchunks < cap ? nchunks : cap;
+  return (unsigned)(g ? g : 1);
+}
+
+cudaError_t launch_count(const CountArgs &a, LoadPath path, const DevInfo &di,
+                         cudaStream_t st) {
+  if (path == LoadPath::kTma) {
+    const unsigned g = grid_for(a.nchunks, (unsigned long long)di.num_sms);
+    pp_tma_kernel<true><<<g, kTmaThreads, kTmaSmemBytes, st>>>(a, nullptr);
+  } else {
+    const unsigned g =
+        grid_for(a.nchunks, (unsigned long long)di.num_sms * di.ldg_blocks_per_sm);
+    pp_count_ldg_kernel<<<g, kLdgThreads, 0, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_readonly(const CountArgs &a, unsigned long long *sink, const DevInfo &di,
+                            cudaStream_t st) {
+  const unsigned g = grid_for(a.nchunks, (unsigned long long)di.num_sms);
+  pp_tma_kernel<false><<<g, kTmaThreads, kTmaSmemBytes, st>>>(a, sink);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_segmented(const SegArgs &a, const DevInfo &di, cudaStream_t st) {
+  if (a.nseg == 0) return cudaSuccess;
+  const unsigned long long warps_per_block = kSegThreads / 32;
+  const unsigned long long need = (a.nseg + warps_per_block - 1) / warps_per_block;
+  const unsigned g = grid_for(need, (unsigned long long)di.num_sms * di.seg_blocks_per_sm);
+  pp_seg_kernel<<<g, kSegThreads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace pp

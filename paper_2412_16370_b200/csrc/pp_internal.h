@@ -1,0 +1,69 @@
+// pp_internal.h — launchers shared between the kernel and C-ABI translation units.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pp {
+
+// Split of one contiguous device byte range into a 16-byte aligned body plus
+// <16-byte head and tail (the reference's head_load / count_tail split,
+// edges.py:32-93, with "aligned" meaning the device address).
+struct CountArgs {
+  const uint8_t *body;
+  unsigned long long body_bytes;  // multiple of 16
+  unsigned long long nchunks;     // ceil(body_bytes / chunk bytes)
+  const uint8_t *head;
+  const uint8_t *tail;
+  uint32_t head_bytes;  // < 16
+  uint32_t tail_bytes;  // < 16
+  unsigned long long *counters;
+  int width;
+  int rot;  // 8 * (address of first byte mod 8), flush_fw's rot (accumulate.py:115-130)
+};
+
+struct SegArgs {
+  const uint8_t *base;
+  const unsigned long long *seg_off;  // nullptr => fixed segments
+  unsigned long long seg_bytes;       // fixed mode only
+  unsigned long long nseg;
+  unsigned long long *out;
+  int width;
+  int overwrite;
+};
+
+enum class LoadPath : int { kTma = 0, kLdg = 1 };
+
+struct DevInfo {
+  int num_sms;
+  int cc_major, cc_minor;
+  int seg_blocks_per_sm;
+  int ldg_blocks_per_sm;
+  bool ready;
+};
+
+cudaError_t device_info(int dev, DevInfo *out);
+
+// Fills head/body/tail fields of a (given data pointer, nbytes, chunk size).
+void split_range(const uint8_t *data, unsigned long long nbytes,
+                 unsigned long long chunk_bytes, CountArgs *a);
+
+unsigned long long count_chunk_bytes(LoadPath path);
+cudaError_t launch_count(const CountArgs &a, LoadPath path, const DevInfo &di,
+                         cudaStream_t st);
+cudaError_t launch_segmented(const SegArgs &a, const DevInfo &di, cudaStream_t st);
+cudaError_t launch_readonly(const CountArgs &a, unsigned long long *sink,
+                            const DevInfo &di, cudaStream_t st);
+
+cudaError_t launch_gen_uniform(uint64_t *dst, unsigned long long nwords, uint64_t seed,
+                               uint64_t word_offset, cudaStream_t st);
+cudaError_t launch_gen_bernoulli(uint64_t *dst, unsigned long long nwords, uint64_t seed,
+                                 uint64_t word_offset, uint32_t q, cudaStream_t st);
+cudaError_t launch_gen_blocks(uint64_t *dst, unsigned long long nwords, uint64_t seed,
+                              uint64_t word_offset, uint64_t block_bytes,
+                              cudaStream_t st);
+cudaError_t launch_gen_onehot32(uint32_t *dst, unsigned long long nwords, uint64_t seed,
+                                uint64_t word_offset, const uint32_t *thr31,
+                                cudaStream_t st);
+
+}  // namespace pp

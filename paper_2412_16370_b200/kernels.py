@@ -1,0 +1,266 @@
+"""The B200 kernel object, the registry and the public entry point.
+
+Mirrors the reference's dispatch layer (/root/reference/pkg/src/pospopcnt/
+kernels.py:48-63, 276-333): same names (``KERNEL_ENV``, ``list_kernels``,
+``get_kernel``, ``select_kernel``, ``pospopcnt``), same error classes, same
+accumulate-into-counters contract.  The registry holds exactly one kernel,
+``"b200"``, whose ``run`` launches the hand-written sm_100a CUDA kernel
+through the C ABI.  It also satisfies the reference's duck-typed kernel
+protocol, so ``pospopcnt_ref.pospopcnt(view, w, kernel=B200Kernel())`` works
+unchanged (kernels.py:329-333).
+
+Data placement:
+  * CUDA tensor, or InputView over one  -> zero-copy, counted in place
+  * host bytes / bytearray / memoryview / numpy / CPU tensor
+                                        -> pp_count_host: pipelined H2D
+                                           copies overlapped with counting
+Counter placement:
+  * CUDA int64/uint64 tensor (>= w entries) -> accumulated on the device,
+    asynchronously on the current stream (no host sync)
+  * list / numpy array / anything indexable -> results read back and added
+    as Python ints (reference semantics, kernels.py:315-333)
+"""
+
+import ctypes
+import os
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .core import (
+    InputView,
+    KernelUnavailableError,
+    UnknownKernelError,
+    W_MAX,
+    check_width,
+    is_torch_tensor,
+    new_counters,
+)
+
+KERNEL_ENV = "POSPOPCNT_KERNEL"
+
+
+@dataclass(frozen=True)
+class KernelDescriptor:
+    """Identity and geometry of a kernel (kernels.py:52-63).
+
+    For the B200 kernel r = 128: each thread's load vector is one 16-byte
+    LDS/LDG.128, and block_bytes = 2r as in the reference.
+    """
+
+    name: str
+    r: int
+    block_bytes: int
+
+    def __post_init__(self):
+        assert self.r >= W_MAX and self.r & (self.r - 1) == 0
+
+
+_tls = threading.local()
+
+
+def _host_u8(base, offset, nbytes):
+    """(pointer, keepalive) for a host buffer slice."""
+    if is_torch_tensor(base):
+        if not base.is_contiguous():
+            raise ValueError("input tensor must be contiguous")
+        return base.data_ptr() + offset, base
+    arr = base if isinstance(base, np.ndarray) else np.frombuffer(
+        memoryview(base).cast("B"), dtype=np.uint8)
+    if isinstance(base, np.ndarray):
+        if not arr.flags.c_contiguous:
+            raise ValueError("input array must be C-contiguous")
+        arr = arr.reshape(-1).view(np.uint8)
+    return arr.ctypes.data + offset, arr
+
+
+def _device_scratch(device):
+    """Per-thread, per-device u64 scratch counters (threads stay independent)."""
+    import torch
+    cache = getattr(_tls, "scratch", None)
+    if cache is None:
+        cache = _tls.scratch = {}
+    t = cache.get(device)
+    if t is None:
+        t = cache[device] = torch.zeros(W_MAX, dtype=torch.int64, device=device)
+    return t
+
+
+def _device_counters(counters, w, device):
+    """counters usable in place on `device`, or None."""
+    if is_torch_tensor(counters) and counters.is_cuda:
+        import torch
+        if counters.device != device:
+            raise ValueError("counters live on a different device than the data")
+        if counters.dtype not in (torch.int64, torch.uint64) or not counters.is_contiguous():
+            raise ValueError("device counters must be a contiguous int64/uint64 tensor")
+        return counters
+    return None
+
+
+def _add_into(counters, values, w):
+    """counters[j] += values[j] with Python-int semantics (reference contract)."""
+    if is_torch_tensor(counters):
+        import torch
+        counters[:w] += torch.as_tensor(np.asarray(values[:w], dtype=np.int64)).to(
+            counters.device, counters.dtype)
+        return
+    for j in range(w):
+        v = int(values[j])
+        if v:
+            counters[j] += v
+
+
+class B200Kernel:
+    """Hand-written sm_100a positional popcount behind the reference protocol."""
+
+    name = "b200"
+    r = 128
+
+    def __init__(self):
+        self.descriptor = KernelDescriptor(self.name, self.r, 2 * self.r)
+        self._avail = None
+
+    def __repr__(self):
+        return f"<kernel {self.name} r={self.r}>"
+
+    def available(self):
+        if self._avail is None:
+            try:
+                info = _lib.device_info(0)
+                self._avail = info["cc"][0] == 10
+            except Exception:  # noqa: BLE001 - unavailable means unavailable
+                self._avail = False
+        return self._avail
+
+    def run(self, view, w, counters, fa=None, probe=None):
+        """Add the positional popcount of ``view`` into ``counters``.
+
+        Like the reference's compiled kernel (kernels.py:243-244) this
+        kernel cannot be instrumented with ``fa`` / ``probe``.
+        """
+        if fa is not None or probe is not None:
+            raise ValueError("the b200 kernel cannot be instrumented")
+        check_width(w)
+        view = InputView.of(view).check_complete(w)
+        if len(counters) < w:
+            raise ValueError(f"counter array holds {len(counters)} < {w} entries")
+        lib = _lib.load()
+        if view.nbytes == 0:
+            return counters
+        if view.on_device:
+            return self._run_device(lib, view, w, counters)
+        return self._run_host(lib, view, w, counters)
+
+    def _run_device(self, lib, view, w, counters):
+        import torch
+        base = view.base
+        if not base.is_contiguous():
+            raise ValueError("input tensor must be contiguous")
+        dev = base.device
+        with torch.cuda.device(dev):
+            stream = torch.cuda.current_stream(dev).cuda_stream
+            ptr = base.data_ptr() + view.offset
+            dc = _device_counters(counters, w, dev)
+            if dc is not None:
+                _lib.check(lib.pp_count(ptr, view.nbytes, w, dc.data_ptr(), stream))
+                return counters
+            scratch = _device_scratch(dev)
+            scratch.zero_()
+            _lib.check(lib.pp_count(ptr, view.nbytes, w, scratch.data_ptr(), stream))
+            vals = scratch[:w].cpu().numpy().view(np.uint64)
+        _add_into(counters, vals, w)
+        return counters
+
+    def _run_host(self, lib, view, w, counters):
+        ptr, keep = _host_u8(view.base, view.offset, view.nbytes)
+        out = np.zeros(W_MAX, dtype=np.uint64)
+        dev_idx = None
+        if is_torch_tensor(counters) and counters.is_cuda:
+            dev_idx = counters.device.index
+        if dev_idx is not None:
+            import torch
+            with torch.cuda.device(dev_idx):
+                _lib.check(lib.pp_count_host(ptr, view.nbytes, w, out.ctypes.data))
+        else:
+            _lib.check(lib.pp_count_host(ptr, view.nbytes, w, out.ctypes.data))
+        del keep
+        _add_into(counters, out, w)
+        return counters
+
+
+_KERNELS = None
+
+
+def _registry():
+    """The one built-in kernel (kernels.py:276-285 holds four CPU kernels)."""
+    global _KERNELS
+    if _KERNELS is None:
+        _KERNELS = [B200Kernel()]
+    return _KERNELS
+
+
+def list_kernels():
+    """All built-in kernels with availability (kernels.py:288-290)."""
+    return [(k.descriptor, k.available()) for k in _registry()]
+
+
+def get_kernel(name):
+    """kernels.py:293-297."""
+    for k in _registry():
+        if k.name == name:
+            return k
+    raise UnknownKernelError(f"unknown kernel {name!r}")
+
+
+def select_kernel(override=None):
+    """Resolve a kernel: explicit override, POSPOPCNT_KERNEL, else widest (kernels.py:300-312).
+
+    Unlike the reference there is nothing to fall back to: if no kernel is
+    available this raises KernelUnavailableError instead of returning None.
+    """
+    name = override or os.environ.get(KERNEL_ENV) or None
+    if name is not None:
+        k = get_kernel(name)
+        if not k.available():
+            raise KernelUnavailableError(f"kernel {name!r} is not available on this host")
+        return k
+    best = None
+    for k in _registry():
+        if k.available() and (best is None or k.r > best.r):
+            best = k
+    if best is None:
+        raise KernelUnavailableError("no pospopcnt kernel is available on this host "
+                                     "(needs an sm_100 GPU and libpospopcnt_b200.so)")
+    return best
+
+
+def pospopcnt(data, width, counters=None, kernel=None):
+    """Add the positional population count of ``data`` to ``counters``.
+
+    Same contract as the reference (kernels.py:315-333): ``data`` is
+    bytes-like, a numpy array, a torch tensor (host or CUDA) or an
+    InputView over any of these; its length must be a multiple of width/8.
+    Returns the counter object (a fresh list when ``counters`` is None).
+    ``kernel`` may be a kernel object, a kernel name, or None.
+    """
+    check_width(width)
+    view = InputView.of(data).check_complete(width)
+    if counters is None:
+        counters = new_counters(width)
+    elif len(counters) < width:
+        raise ValueError(f"counter array holds {len(counters)} < {width} entries")
+    if kernel is None or isinstance(kernel, str):
+        kernel = select_kernel(kernel)
+    elif not kernel.available():
+        raise KernelUnavailableError(f"kernel {kernel.name!r} is not available on this host")
+    return kernel.run(view, width, counters)
+
+
+def count_device(ptr, nbytes, width, counters_ptr, stream=0):
+    """Raw device-pointer entry (pp_count), for callers managing their own memory."""
+    lib = _lib.load()
+    _lib.check(lib.pp_count(ctypes.c_void_p(ptr), nbytes, width,
+                            ctypes.c_void_p(counters_ptr), ctypes.c_void_p(stream)))

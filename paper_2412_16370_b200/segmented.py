@@ -1,0 +1,116 @@
+"""Segmented (many-small-arrays) counting: one launch, one counter row per array.
+
+New relative to the reference, which counts one array per call
+(kernels.py:315-333) and takes its short-array path for anything below 15
+vectors (edges.py:96-102, kernels.py:249-250).  Calling the reference once
+per segment and collecting each counter list is the semantics reproduced
+here: row s of the output equals ``pospopcnt(segment_s, width)``.
+
+Segments live in one CUDA byte buffer; segment s is bytes
+[offsets[s], offsets[s+1]) of the view.  Every segment must be word-complete.
+"""
+
+import numpy as np
+
+from . import _lib
+from .core import InputLengthError, InputView, check_width, is_torch_tensor
+
+
+def _device_view(data):
+    view = InputView.of(data)
+    if not view.on_device:
+        raise ValueError("segmented counting needs the data in a CUDA tensor "
+                         "(copy it once with torch.as_tensor(...).cuda())")
+    if not view.base.is_contiguous():
+        raise ValueError("input tensor must be contiguous")
+    return view
+
+
+def _out_tensor(out, nseg, width, device):
+    import torch
+    if out is None:
+        return torch.zeros((nseg, width), dtype=torch.int64, device=device), True
+    if not (is_torch_tensor(out) and out.is_cuda and out.device == device):
+        raise ValueError("out must be a CUDA tensor on the data's device")
+    if out.dtype not in (torch.int64, torch.uint64) or not out.is_contiguous():
+        raise ValueError("out must be a contiguous int64/uint64 tensor")
+    if out.numel() < nseg * width:
+        raise ValueError(f"out holds {out.numel()} < {nseg * width} counters")
+    return out, False
+
+
+def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validate=True):
+    """Positional counts of many arrays in one launch.
+
+    ``offsets``: nseg+1 non-decreasing byte offsets into the view (host
+    sequence / numpy array, or a CUDA int64 tensor).  ``out``: CUDA
+    (nseg, width) int64 tensor accumulated into (or overwritten when
+    ``accumulate=False``); allocated zeroed when None.  Returns ``out``.
+    Asynchronous on the current stream.
+    """
+    import torch
+    check_width(width)
+    view = _device_view(data)
+    dev = view.base.device
+    step = width // 8
+    if is_torch_tensor(offsets) and offsets.is_cuda:
+        offs = offsets.to(torch.int64).contiguous()
+        if validate and offs.numel() > 1:
+            d = offs[1:] - offs[:-1]
+            bad_order = bool((d < 0).any()) or int(offs[0]) < 0 or int(offs[-1]) > view.nbytes
+            if bad_order:
+                raise ValueError("offsets must be non-decreasing and inside the view")
+            if bool((d % step != 0).any()):
+                raise InputLengthError(f"a segment is not a multiple of the {step}-byte word size")
+    else:
+        offs_np = np.asarray(offsets, dtype=np.int64)
+        if offs_np.ndim != 1 or offs_np.size < 1:
+            raise ValueError("offsets must be a 1-D sequence of nseg+1 byte offsets")
+        if validate:
+            d = np.diff(offs_np)
+            if (d < 0).any() or offs_np[0] < 0 or offs_np[-1] > view.nbytes:
+                raise ValueError("offsets must be non-decreasing and inside the view")
+            if (d % step).any():
+                raise InputLengthError(f"a segment is not a multiple of the {step}-byte word size")
+        offs = torch.as_tensor(offs_np, device=dev)
+    nseg = offs.numel() - 1
+    out, fresh = _out_tensor(out, max(nseg, 0), width, dev)
+    if nseg <= 0:
+        return out
+    lib = _lib.load()
+    flags = _lib.PP_SEG_ACCUMULATE if (accumulate and not fresh) else _lib.PP_SEG_OVERWRITE
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        base_ptr = view.base.data_ptr() + view.offset
+        _lib.check(lib.pp_count_segmented(base_ptr, offs.data_ptr(), nseg, width,
+                                          out.data_ptr(), flags, stream))
+        # keep the offsets tensor alive until the kernel has consumed it
+        offs.record_stream(torch.cuda.current_stream(dev))
+    return out
+
+
+def pospopcnt_fixed(data, seg_bytes, width, out=None, accumulate=True):
+    """Equal-size segments: segment s = bytes [s*seg_bytes, (s+1)*seg_bytes) of the view.
+
+    A trailing partial segment is not counted (nseg = nbytes // seg_bytes).
+    """
+    import torch
+    check_width(width)
+    if seg_bytes <= 0:
+        raise ValueError("seg_bytes must be positive")
+    if seg_bytes % (width // 8):
+        raise InputLengthError(f"{seg_bytes} bytes is not a multiple of the "
+                               f"{width // 8}-byte word size")
+    view = _device_view(data)
+    dev = view.base.device
+    nseg = view.nbytes // seg_bytes
+    out, fresh = _out_tensor(out, nseg, width, dev)
+    if nseg == 0:
+        return out
+    lib = _lib.load()
+    flags = _lib.PP_SEG_ACCUMULATE if (accumulate and not fresh) else _lib.PP_SEG_OVERWRITE
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(lib.pp_count_fixed(view.base.data_ptr() + view.offset, seg_bytes, nseg,
+                                      width, out.data_ptr(), flags, stream))
+    return out

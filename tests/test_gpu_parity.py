@@ -1,0 +1,286 @@
+"""GPU parity: the sm_100a path (through the C ABI) vs the CPU oracle.
+
+Bit-exact integer counts are the bar.  Cases mirror the reference's own
+kernel and acceptance tests (pkg/tests/test_kernels.py, test_acceptance.py):
+known answers, length x offset sweeps, alignment / adjacent-memory
+invariance, streaming = batch, conservation, the all-ones overflow check
+(scaled past 2^32 words), and the BASELINE configs at full size.
+"""
+
+import ctypes
+import threading
+
+import numpy as np
+import pytest
+
+from conftest import oracle_bits
+
+pytestmark = pytest.mark.gpu
+
+MIB = 1 << 20
+
+
+def dev_bytes(torch, data, offset=0, pad=0, fill=0):
+    """Place host bytes at `offset` inside a padded CUDA buffer; returns (buf, view)."""
+    import paper_2412_16370_b200 as pp
+    raw = np.frombuffer(bytes(data), dtype=np.uint8)
+    host = np.full(offset + raw.size + pad, fill, dtype=np.uint8)
+    host[offset:offset + raw.size] = raw
+    buf = torch.from_numpy(host).cuda()
+    return buf, pp.InputView(buf, offset, raw.size)
+
+
+def count(torch, pp, view, w):
+    c = torch.zeros(w, dtype=torch.int64, device="cuda")
+    pp.pospopcnt(view, w, counters=c)
+    return [int(x) for x in c.cpu().numpy().view(np.uint64)]
+
+
+# ----------------------------------------------------------- known answers
+def test_known_answers(cuda):
+    torch, pp = cuda
+    assert pp.pospopcnt(torch.tensor([1, 128], dtype=torch.uint8).cuda(), 16) == \
+        [1] + [0] * 14 + [1]
+    assert pp.pospopcnt(torch.tensor([255, 255], dtype=torch.uint8).cuda(), 16) == [1] * 16
+    assert pp.pospopcnt(torch.tensor([0xFF, 0x00, 0x81], dtype=torch.uint8).cuda(), 8) == \
+        [2, 1, 1, 1, 1, 1, 1, 2]
+    assert pp.pospopcnt(torch.tensor([0x0F], dtype=torch.uint8).cuda(), 8) == \
+        [1, 1, 1, 1, 0, 0, 0, 0]
+    for n in (1, 1000, 1_000_000):
+        buf, view = dev_bytes(torch, b"\x01\x80" * n)
+        assert count(torch, pp, view, 16) == [n] + [0] * 14 + [n], n
+    z = torch.zeros(16 * 1024, dtype=torch.uint8, device="cuda")
+    for w in (8, 16, 32, 64):
+        assert pp.pospopcnt(z, w) == [0] * w
+        assert pp.pospopcnt(z[:0], w) == [0] * w
+
+
+def test_host_bytes_entry(cuda, rng):
+    """bytes / bytearray / memoryview / numpy go through the pipelined host path."""
+    torch, pp = cuda
+    raw = rng.randbytes(100_000)
+    want = oracle_bits(raw, 8)
+    for data in (raw, bytearray(raw), memoryview(raw), np.frombuffer(raw, np.uint8)):
+        assert pp.pospopcnt(data, 8) == want
+    c = [1] * 8
+    pp.pospopcnt(raw, 8, counters=c)
+    assert c == [v + 1 for v in want]
+    big = np.frombuffer(rng.randbytes(70 * MIB + 24), np.uint8)  # > 2 staging chunks
+    from oracle import oracle as O
+    assert pp.pospopcnt(pp.InputView(big, 3, 70 * MIB + 16), 16) == \
+        O.hs512(big, 3, 70 * MIB + 16, 16, threads=8)
+
+
+# ------------------------------------------------- sweeps vs the oracle
+@pytest.mark.parametrize("w", (8, 16, 32, 64))
+def test_spot_sweep_lengths_offsets(cuda, oracle, rng, w):
+    """test_kernels.py:40-50 sizes plus chunk-boundary sizes of the B200 kernel."""
+    torch, pp = cuda
+    step = w // 8
+    data = rng.randbytes(3 * (1 << 16) + 200)
+    host = np.frombuffer(data, np.uint8)
+    buf = torch.from_numpy(host.copy()).cuda()
+    sizes = [0, step, 5 * step, 119, 120, 121, 960, 1024, 2048, 2944, 4096, 32768 - 8,
+             32768, 32768 + 8, 65536, 65536 + 24, 3 * (1 << 16)]
+    for n in sizes:
+        n -= n % step
+        for off in (0, 1, 3, 7, 9, 15, 16, 63):
+            if off + n > len(data):
+                continue
+            want = oracle.hs512(host, off, n, w)
+            got = count(torch, pp, pp.InputView(buf, off, n), w)
+            assert got == want, (w, n, off)
+
+
+def test_alignment_invariance_and_poison(cuda, rng):
+    """test_kernels.py:75-91: offset and adjacent bytes never change the result."""
+    torch, pp = cuda
+    payload = rng.randbytes(70_000)
+    want = oracle_bits(payload, 8)
+    for off in range(0, 64, 5):
+        for fill in (0x00, 0xFF, 0xA5):
+            buf, view = dev_bytes(torch, payload, off, pad=37, fill=fill)
+            assert count(torch, pp, view, 8) == want, (off, fill)
+
+
+def test_streaming_equals_batch(cuda, oracle, rng):
+    """test_kernels.py:65-72 / acceptance c5: split counts add up exactly."""
+    torch, pp = cuda
+    data = rng.randbytes(1 << 20)
+    buf = torch.from_numpy(np.frombuffer(data, np.uint8).copy()).cuda()
+    want = oracle.hs512(data, 0, len(data), 16)
+    for split in (0, 2, 722, 2048, 32768 + 6, 1 << 19, 1 << 20):
+        c = torch.zeros(16, dtype=torch.int64, device="cuda")
+        pp.pospopcnt(pp.InputView(buf, 0, split), 16, counters=c)
+        pp.pospopcnt(pp.InputView(buf, split, len(data) - split), 16, counters=c)
+        assert [int(x) for x in c.cpu()] == want, split
+
+
+def test_conservation_random_cases(cuda, rng):
+    """acceptance c5 conservation: sum of counters = popcount of the input."""
+    torch, pp = cuda
+    for case in range(200):
+        w = (8, 16, 32, 64)[case % 4]
+        n = rng.randrange(0, 200_000 // (w // 8) + 1) * (w // 8)
+        data = rng.randbytes(n)
+        off = rng.randrange(0, 16)
+        buf, view = dev_bytes(torch, data, off, pad=rng.randrange(0, 9), fill=0xFF)
+        got = count(torch, pp, view, w)
+        assert sum(got) == int.from_bytes(data, "little").bit_count(), (w, n, off)
+
+
+# --------------------------------------------------------- exactness at scale
+def test_all_ones_past_2_32_words(cuda):
+    """acceptance c4 (256 MiB all-ones at w=16) scaled to 5 GiB at w=8:
+    every counter is 5*2^30 > 2^32, so any 32-bit truncation shows."""
+    torch, pp = cuda
+    buf = torch.full((256 * MIB,), 0xFF, dtype=torch.uint8, device="cuda")
+    c = torch.zeros(16, dtype=torch.int64, device="cuda")
+    pp.pospopcnt(buf, 16, counters=c)
+    assert [int(x) for x in c.cpu()] == [134_217_728] * 16
+    del buf
+    n = 5 << 30
+    big = torch.full((n,), 0xFF, dtype=torch.uint8, device="cuda")
+    c = torch.zeros(8, dtype=torch.int64, device="cuda")
+    pp.pospopcnt(big, 8, counters=c)
+    assert [int(x) for x in c.cpu()] == [n] * 8
+    del big
+    torch.cuda.empty_cache()
+
+
+def test_generators_match_cpu_twins(cuda, oracle):
+    torch, pp = cuda
+    from paper_2412_16370_b200 import gen
+    n = 1 << 16
+    for off in (0, 12345):
+        assert np.array_equal(gen.generate("uniform", n, 7, word_offset=off).cpu().numpy(),
+                              oracle.gen_uniform(n, 7, off))
+        assert np.array_equal(gen.generate("bernoulli", n, 8, word_offset=off, q=655).cpu().numpy(),
+                              oracle.gen_bernoulli(n, 8, 655, off))
+        assert np.array_equal(gen.generate("blocks", n, 9, word_offset=off,
+                                           block_bytes=4096).cpu().numpy(),
+                              oracle.gen_blocks(n, 9, 4096, off))
+        assert np.array_equal(gen.generate("onehot32", n, 10, word_offset=off).cpu().numpy(),
+                              oracle.gen_onehot32(n, 10, word_offset=off))
+    ones = gen.generate("bernoulli", 4096, 1, q=65536).cpu().numpy()
+    assert (ones == 0xFF).all()
+
+
+def _full_size(torch, pp, oracle, kind, nbytes, w, seed, **kw):
+    from paper_2412_16370_b200 import gen
+    buf = gen.generate(kind, nbytes, seed, **kw)
+    c = torch.zeros(w, dtype=torch.int64, device="cuda")
+    pp.pospopcnt(buf, w, counters=c)
+    got = [int(x) for x in c.cpu()]
+    host = buf.cpu().numpy()
+    del buf
+    return got, host
+
+
+def test_config_c1_w16_2mib(cuda, oracle):
+    torch, pp = cuda
+    got, host = _full_size(torch, pp, oracle, "uniform", 2 * MIB, 16, 0xC1)
+    assert got == oracle.hs512(host, 0, host.size, 16)
+    assert got == oracle.scalar(host, 16)
+
+
+def test_config_c2_w8_1gib(cuda, oracle):
+    torch, pp = cuda
+    got, host = _full_size(torch, pp, oracle, "uniform", 1 << 30, 8, 0xC2)
+    assert got == oracle.hs512(host, 0, host.size, 8, threads=16)
+
+
+def test_config_c3_w32_onehot_4gib(cuda, oracle):
+    torch, pp = cuda
+    nbytes = 4 << 30
+    got, host = _full_size(torch, pp, oracle, "onehot32", nbytes, 32, 0xC3)
+    assert sum(got) == nbytes // 4  # exactly one bit per word
+    assert got == oracle.hs512(host, 0, host.size, 32, threads=16)
+    assert got[0] > got[1] > got[8] > got[31] > 0  # Zipf-shaped
+
+
+def test_config_c4_w64_short_unaligned(cuda, oracle):
+    torch, pp = cuda
+    from paper_2412_16370_b200 import gen
+    lengths = (1, 3, 17, 255, 512, 8192, 131072, 8388608)
+    buf = gen.generate("bernoulli", 64 * MIB + 64, 0xC4, q=655)
+    host = buf.cpu().numpy()
+    for n in lengths:
+        for off in range(1, 8):
+            nb = 8 * n
+            got = count(torch, pp, pp.InputView(buf, off, nb), 64)
+            assert got == oracle.hs512(host, off, nb, 64, threads=8), (n, off)
+
+
+def test_config_c5_shard_w16(cuda, oracle):
+    """One 1 GiB shard of the 64 GiB C5 array (word_offset places it mid-array)."""
+    torch, pp = cuda
+    got, host = _full_size(torch, pp, oracle, "blocks", 1 << 30, 16, 0xC5,
+                           word_offset=(3 << 30) // 8)
+    assert got == oracle.hs512(host, 0, host.size, 16, threads=16)
+
+
+# ----------------------------------------------------------- API behaviour
+def test_device_counters_accumulate_and_errors(cuda, rng):
+    torch, pp = cuda
+    data = rng.randbytes(4096)
+    buf, view = dev_bytes(torch, data)
+    c = torch.ones(8, dtype=torch.int64, device="cuda")
+    pp.pospopcnt(view, 8, counters=c)
+    pp.pospopcnt(view, 8, counters=c)
+    want = oracle_bits(data, 8)
+    assert [int(x) for x in c.cpu()] == [1 + 2 * v for v in want]
+    with pytest.raises(pp.InputLengthError):
+        pp.pospopcnt(buf[:7], 64)
+    with pytest.raises(ValueError):
+        pp.pospopcnt(buf, 12)
+    with pytest.raises(ValueError):
+        pp.pospopcnt(buf, 16, counters=[0] * 8)
+    longer = [0] * 20
+    pp.pospopcnt(view, 16, counters=longer)
+    assert longer[16:] == [0] * 4
+
+
+def test_c_abi_rejects_host_pointers(cuda):
+    torch, pp = cuda
+    from paper_2412_16370_b200 import _lib
+    lib = _lib.load()
+    host = np.zeros(64, dtype=np.uint8)
+    dc = torch.zeros(8, dtype=torch.int64, device="cuda")
+    rc = lib.pp_count(host.ctypes.data, 64, 8, dc.data_ptr(), None)
+    assert rc == _lib.PP_EARG
+    assert b"device" in lib.pp_last_error() or b"CUDA" in lib.pp_last_error()
+    rc = lib.pp_count(dc.data_ptr(), 64, 12, dc.data_ptr(), None)
+    assert rc == _lib.PP_EWIDTH
+
+
+def test_concurrent_threads_distinct_counters(cuda, rng):
+    """test_kernels.py:233-253."""
+    torch, pp = cuda
+    data = rng.randbytes(1 << 20)
+    want = oracle_bits(data[:4096], 16)
+    full_want = None
+    from oracle import oracle as O
+    full_want = O.hs512(data, 0, len(data), 16)
+    buf, view = dev_bytes(torch, data)
+    results, errors = [], []
+
+    def work(use_host):
+        try:
+            outs = []
+            for _ in range(5):
+                if use_host:
+                    outs.append(pp.pospopcnt(data, 16))
+                else:
+                    outs.append(pp.pospopcnt(view, 16))
+            results.append(all(o == full_want for o in outs))
+        except Exception as exc:  # pragma: no cover
+            errors.append(exc)
+
+    ths = [threading.Thread(target=work, args=(i % 2 == 0,)) for i in range(6)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errors and all(results) and len(results) == 6
+    assert want == oracle_bits(data[:4096], 16)

@@ -1,0 +1,110 @@
+"""GPU parity of the segmented (many-small-arrays) mode vs the CPU oracle.
+
+Row s must equal the reference's count of segment s alone
+(NumbaKernel.run on InputView(base, off[s], len_s), kernels.py:242-270).
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_c1_exhaustive_sweep_via_segments(cuda, oracle):
+    """acceptance c1 (pkg/tests/test_acceptance.py:41-64): lengths 0..4096 x
+    alignments 0..63 x every width, each case one segment of one launch.
+    Case (a, n) is placed at device address = a mod 64 between poison gaps."""
+    torch, pp = cuda
+    import random
+    rng = random.Random(20240)
+    src = np.frombuffer(rng.randbytes(64 + 4096), np.uint8)
+    from paper_2412_16370_b200 import _lib
+    lib = _lib.load()
+    for w in (8, 16, 32, 64):
+        step = w // 8
+        slot = 64 + 4096 + 64
+        lens = np.arange(0, 4097, step)
+        cases = [(a, int(n)) for a in range(64) for n in lens]
+        host = np.full(len(cases) * slot, 0xA5, dtype=np.uint8)
+        offs = np.empty(3 * len(cases) + 1, dtype=np.int64)
+        real_rows = np.arange(len(cases)) * 3 + 1
+        exp_offs = []
+        for i, (a, n) in enumerate(cases):
+            s = i * slot
+            host[s + a:s + a + n] = src[a:a + n]
+            offs[3 * i] = s
+            offs[3 * i + 1] = s + a
+            offs[3 * i + 2] = s + a + n
+            exp_offs.append((s + a, s + a + n))
+        offs[-1] = len(cases) * slot
+        buf = torch.from_numpy(host).cuda()
+        doffs = torch.from_numpy(offs).cuda()
+        out = torch.zeros((3 * len(cases), w), dtype=torch.int64, device="cuda")
+        rc = lib.pp_count_segmented(buf.data_ptr(), doffs.data_ptr(), 3 * len(cases), w,
+                                    out.data_ptr(), _lib.PP_SEG_OVERWRITE, None)
+        _lib.check(rc)
+        got = out.cpu().numpy().view(np.uint64)[real_rows]
+        # oracle: the same views of the same bytes
+        o = np.array([x for ab in exp_offs for x in ab], dtype=np.uint64)
+        # segments() wants a CSR partition; evaluate real views pairwise
+        want = np.zeros_like(got)
+        for k in range(0, len(exp_offs), 4096):
+            chunk = exp_offs[k:k + 4096]
+            pair = np.array([v for ab in chunk for v in ab], dtype=np.uint64)
+            rows = oracle.segments(host, pair, w)[0::2]
+            want[k:k + len(chunk)] = rows
+        assert np.array_equal(got, want), w
+        del o
+
+
+def test_ragged_random_segments_poison(cuda, oracle, rng):
+    torch, pp = cuda
+    for w in (8, 16, 32, 64):
+        step = w // 8
+        lens = [rng.choice((0, step, 3 * step, 100 * step, rng.randrange(0, 9000) // step * step,
+                            rng.randrange(0, 300_000) // step * step)) for _ in range(3000)]
+        offs = np.zeros(len(lens) + 1, dtype=np.int64)
+        offs[1:] = np.cumsum(lens)
+        base = 5  # misaligned start of the whole batch
+        host = np.frombuffer(rng.randbytes(int(offs[-1]) + base + 11), np.uint8).copy()
+        buf = torch.from_numpy(host).cuda()
+        view = pp.InputView(buf, base, int(offs[-1]))
+        out = pp.pospopcnt_segmented(view, offs, w)
+        want = oracle.segments(host, (offs + base).astype(np.uint64), w)
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), want), w
+        # accumulate semantics
+        pp.pospopcnt_segmented(view, offs, w, out=out)
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), 2 * want), w
+        pp.pospopcnt_segmented(view, offs, w, out=out, accumulate=False)
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), want), w
+
+
+def test_config_c4_segmented_batch(cuda, oracle):
+    """262,144 independent 4 KiB arrays of Bernoulli(0.01) bits, w=64."""
+    torch, pp = cuda
+    from paper_2412_16370_b200 import gen
+    nseg, seg = 262_144, 4096
+    buf = gen.generate("bernoulli", nseg * seg, 0xC4 + 1, q=655)
+    out = pp.pospopcnt_fixed(buf, seg, 64)
+    got = out.cpu().numpy().view(np.uint64)
+    host = buf.cpu().numpy()
+    offs = np.arange(nseg + 1, dtype=np.uint64) * seg
+    want = oracle.segments(host, offs, 64)
+    assert np.array_equal(got, want)
+    # the fixed and CSR entry points agree
+    out2 = pp.pospopcnt_segmented(buf, offs.astype(np.int64), 64)
+    assert np.array_equal(out2.cpu().numpy().view(np.uint64), want)
+
+
+def test_segment_errors(cuda):
+    torch, pp = cuda
+    buf = torch.zeros(100, dtype=torch.uint8, device="cuda")
+    with pytest.raises(pp.InputLengthError):
+        pp.pospopcnt_segmented(buf, [0, 3, 8], 16)
+    with pytest.raises(ValueError):
+        pp.pospopcnt_segmented(buf, [0, 8, 4], 8)
+    with pytest.raises(ValueError):
+        pp.pospopcnt_segmented(buf, [0, 200], 8)
+    with pytest.raises(pp.InputLengthError):
+        pp.pospopcnt_fixed(buf, 3, 16)
+    assert pp.pospopcnt_segmented(buf, [0], 8).shape == (0, 8)
