@@ -74,61 +74,83 @@ def load_traffic(kernel_key):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled (NVML, ~1 ms period) while the
+    timed region runs; mark() brackets the region on the host clock.  Falls
+    back to one nvidia-smi query per sample if NVML is unavailable."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {  # NVML clocks-event-reason bits
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+        0x4: "sw_power_cap",
+    }
 
-    def __init__(self, index):
-        self.index = index
-        self.proc = None
-        self.lines = []
+    def __init__(self, index, period=0.001):
+        self.index, self.period = index, period
+        self.samples = []  # (t, sm_mhz, reasons_mask)
+        self.t0 = self.t1 = None
+        self.stop = threading.Event()
+        self.max_mhz = None
+        self.nvml = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
         except Exception:  # noqa: BLE001
-            self.proc = None
+            self.nvml = None
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _sample(self):
+        if self.nvml is not None:
+            p = self.nvml
+            return (p.nvmlDeviceGetClockInfo(self.h, p.NVML_CLOCK_SM),
+                    p.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+        out = subprocess.run(
+            ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm",
+             "--format=csv,noheader,nounits"], capture_output=True, text=True).stdout
+        sm, mx = (float(x) for x in out.strip().split(","))
+        self.max_mhz = mx
+        return sm, 0
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                sm, mask = self._sample()
+                self.samples.append((time.perf_counter(), sm, mask))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def mark(self, start):
+        if start:
+            self.t0 = time.perf_counter()
+        else:
+            self.t1 = time.perf_counter()
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:  # noqa: BLE001
-                self.proc.kill()
-            self.t.join(timeout=2)
+        self.stop.set()
+        self.th.join(timeout=2)
 
     def summary(self):
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
-            except ValueError:
-                continue
-            for name, val in zip(names, parts[4:8]):
-                if val.lower() == "active":
+        inside = [s for s in self.samples
+                  if self.t0 is not None and self.t1 is not None and self.t0 <= s[0] <= self.t1]
+        window = "timed region"
+        if not inside:  # region shorter than one sample period: nearest samples
+            inside = sorted(self.samples, key=lambda s: abs(s[0] - (self.t0 or 0)))[:3]
+            window = "nearest samples to the timed region"
+        reasons = set()
+        for _, _, mask in inside:
+            for bit, name in self.REASONS.items():
+                if mask & bit:
                     reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax),
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median([s[1] for s in inside]) if inside else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+                "samples": len(inside), "window": window,
+                "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 def host_threads():
@@ -268,30 +290,32 @@ def main_gpu(args):
         dist.barrier()
     torch.cuda.synchronize()
 
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        time.sleep(0.25 if args.steps >= 10 else 0.0)
+        time.sleep(0.05)  # let the sampler start before the timed region
+        clk.mark(True)
         e0.record(st)
-        for i in range(args.steps):
-            ev[i][0].record(st)
-            if seg_out is not None:
-                _lib.check(lib.pp_count_fixed(view_ptr, 4096, nbytes // 4096, w,
-                                              seg_out.data_ptr(), _lib.PP_SEG_OVERWRITE, sp))
-            else:
-                _lib.check(lib.pp_count(view_ptr, nbytes, w, counters.data_ptr(), sp))
-            ev[i][1].record(st)
-            if world > 1:
-                glob.copy_(counters)
-                dist.all_reduce(glob)
+        for _ in range(args.steps):
+            step()
         e1.record(st)
         torch.cuda.synchronize()
+        clk.mark(False)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t_ms = e0.elapsed_time(e1)
-    k_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    if world == 1:
+        # each step is exactly one launch of the dominant kernel
+        k_ms = t_ms / args.steps
+    else:
+        # kernel alone (no allreduce between launches), same stream, same clocks
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record(st)
+        for _ in range(args.steps):
+            _lib.check(lib.pp_count(view_ptr, nbytes, w, counters.data_ptr(), sp))
+        k1.record(st)
+        torch.cuda.synchronize()
+        k_ms = k0.elapsed_time(k1) / args.steps
     if world > 1:
         tt = torch.tensor([t_ms, k_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -306,7 +330,7 @@ def main_gpu(args):
         host = buf.cpu().numpy()
         want = O.hs512(host, offset, nbytes, w, threads=host_threads())
         got = counters.cpu().numpy().view(np.uint64)[:w]
-        total = args.warmup + args.steps
+        total = args.warmup + args.steps + (args.steps if world > 1 else 0)
         exact = bool(all(int(g) == total * x for g, x in zip(got, want)))
         del host
 

@@ -55,6 +55,7 @@ def lib():
         L.oracle_hs512.argtypes = [u8p, sz, sz, ctypes.c_int, u8p]
         L.oracle_hs512_mt.argtypes = [u8p, sz, sz, ctypes.c_int, u8p, ctypes.c_int]
         L.oracle_segments.argtypes = [u8p, u8p, sz, ctypes.c_int, u8p, ctypes.c_int]
+        L.oracle_views.argtypes = [u8p, u8p, u8p, sz, ctypes.c_int, u8p, ctypes.c_int]
         L.oracle_gen_uniform.argtypes = [u8p, sz, u64, u64]
         L.oracle_gen_bernoulli.argtypes = [u8p, sz, u64, u64, ctypes.c_uint32]
         L.oracle_gen_blocks.argtypes = [u8p, sz, u64, u64, u64]
@@ -119,6 +120,22 @@ def segments(base, offsets, w, threads=None):
     threads = threads or len(os.sched_getaffinity(0))
     _check(lib().oracle_segments(a.ctypes.data, offs.ctypes.data, nseg, w, out.ctypes.data,
                                  threads))
+    return out
+
+
+def views(base, starts, ends, w, threads=None):
+    """Row s = NumbaKernel.run(InputView(base, starts[s], ends[s]-starts[s]), w)."""
+    a = _u8(base)
+    st = np.ascontiguousarray(starts, dtype=np.uint64)
+    en = np.ascontiguousarray(ends, dtype=np.uint64)
+    if st.shape != en.shape or (en < st).any() or (en.size and en.max() > a.size):
+        raise ValueError("bad views")
+    out = np.zeros((st.size, w), dtype=np.uint64)
+    if st.size == 0:
+        return out
+    threads = threads or len(os.sched_getaffinity(0))
+    _check(lib().oracle_views(a.ctypes.data, st.ctypes.data, en.ctypes.data, st.size, w,
+                              out.ctypes.data, threads))
     return out
 
 

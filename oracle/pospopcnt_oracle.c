@@ -303,7 +303,7 @@ int oracle_hs512_mt(const uint8_t *base, size_t offset, size_t n, int w, uint64_
  * [seg_off[s], seg_off[s+1]) (each a base-relative InputView), threaded. */
 typedef struct {
   const uint8_t *base;
-  const uint64_t *seg_off;
+  const uint64_t *starts, *ends;
   size_t s0, s1;
   int w;
   uint64_t *out;
@@ -313,15 +313,16 @@ typedef struct {
 static void *seg_main(void *arg) {
   segjob_t *j = (segjob_t *)arg;
   for (size_t s = j->s0; s < j->s1; ++s) {
-    const uint64_t a = j->seg_off[s], b = j->seg_off[s + 1];
+    const uint64_t a = j->starts[s], b = j->ends[s];
     int rc = oracle_hs512(j->base, a, b - a, j->w, j->out + s * (size_t)j->w);
     if (rc) j->rc = rc;
   }
   return NULL;
 }
 
-int oracle_segments(const uint8_t *base, const uint64_t *seg_off, size_t nseg, int w,
-                    uint64_t *out, int nthreads) {
+/* Arbitrary views [starts[s], ends[s]) of one buffer, threaded. */
+int oracle_views(const uint8_t *base, const uint64_t *starts, const uint64_t *ends, size_t nseg,
+                 int w, uint64_t *out, int nthreads) {
   if (nthreads < 1) nthreads = 1;
   if ((size_t)nthreads > nseg) nthreads = nseg ? (int)nseg : 1;
   segjob_t *jobs = (segjob_t *)calloc((size_t)nthreads, sizeof(segjob_t));
@@ -333,7 +334,8 @@ int oracle_segments(const uint8_t *base, const uint64_t *seg_off, size_t nseg, i
   }
   for (int t = 0; t < nthreads; ++t) {
     jobs[t].base = base;
-    jobs[t].seg_off = seg_off;
+    jobs[t].starts = starts;
+    jobs[t].ends = ends;
     jobs[t].s0 = nseg * (size_t)t / (size_t)nthreads;
     jobs[t].s1 = nseg * (size_t)(t + 1) / (size_t)nthreads;
     jobs[t].w = w;
@@ -348,6 +350,12 @@ int oracle_segments(const uint8_t *base, const uint64_t *seg_off, size_t nseg, i
   free(jobs);
   free(th);
   return rc;
+}
+
+/* CSR partition: segment s = [seg_off[s], seg_off[s+1]). */
+int oracle_segments(const uint8_t *base, const uint64_t *seg_off, size_t nseg, int w,
+                    uint64_t *out, int nthreads) {
+  return oracle_views(base, seg_off, seg_off + 1, nseg, w, out, nthreads);
 }
 
 /* ---------------------------------------------------------- generators

@@ -6,7 +6,7 @@
 //   pp_count_tma_kernel   persistent, one CTA per SM.  One elected producer
 //                         thread streams 32 KiB chunks of the aligned body
 //                         HBM -> shared memory with cp.async.bulk (UBLKCP),
-//                         NSTAGE-deep mbarrier ring; 8 consumer warps read
+//                         3-deep mbarrier ring; 8 consumer warps read
 //                         the stage with conflict-free LDS.128 and run the
 //                         two-level carry-save count (pp_device.cuh).
 //   pp_count_ldg_kernel   same arithmetic fed by LDG.128 straight to
@@ -23,7 +23,7 @@
 namespace pp {
 
 constexpr int kTmaConsumerWarps = 8;
-constexpr int kTmaStages = 6;
+constexpr int kTmaStages = 3;  // 3 x 32 KiB: best of the scripts/bw_probe.cu sweep (profiles/)
 constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
 constexpr int kTmaStageVecs = kTmaConsumerWarps * 32 * 8;  // 2048 x 16 B = 32 KiB
 constexpr unsigned long long kTmaStageBytes = kTmaStageVecs * 16ull;

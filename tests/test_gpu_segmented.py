@@ -10,6 +10,16 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+def golden_digest(name):
+    import json
+    import os
+    p = os.path.join(os.path.dirname(__file__), "golden", "golden.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        return json.load(f)["digests"].get(name)
+
+
 def test_c1_exhaustive_sweep_via_segments(cuda, oracle):
     """acceptance c1 (pkg/tests/test_acceptance.py:41-64): lengths 0..4096 x
     alignments 0..63 x every width, each case one segment of one launch.
@@ -45,16 +55,16 @@ def test_c1_exhaustive_sweep_via_segments(cuda, oracle):
         _lib.check(rc)
         got = out.cpu().numpy().view(np.uint64)[real_rows]
         # oracle: the same views of the same bytes
-        o = np.array([x for ab in exp_offs for x in ab], dtype=np.uint64)
-        # segments() wants a CSR partition; evaluate real views pairwise
-        want = np.zeros_like(got)
-        for k in range(0, len(exp_offs), 4096):
-            chunk = exp_offs[k:k + 4096]
-            pair = np.array([v for ab in chunk for v in ab], dtype=np.uint64)
-            rows = oracle.segments(host, pair, w)[0::2]
-            want[k:k + len(chunk)] = rows
+        st = np.array([a for a, _ in exp_offs], dtype=np.uint64)
+        en = np.array([b for _, b in exp_offs], dtype=np.uint64)
+        want = oracle.views(host, st, en, w)
         assert np.array_equal(got, want), w
-        del o
+        # and against the reference's own outputs (golden digest, make_golden.py)
+        dig = golden_digest(f"c1_sweep_w{w}")
+        if dig is not None:
+            import hashlib
+            assert hashlib.sha256(np.ascontiguousarray(got).tobytes()).hexdigest() == \
+                dig["sha256_u64_rows"], w
 
 
 def test_ragged_random_segments_poison(cuda, oracle, rng):
