@@ -55,6 +55,9 @@ extern "C" {
 /* flags for the segmented entry points */
 #define PP_SEG_ACCUMULATE 0  /* out[s*w+j] += count (reference semantics)  */
 #define PP_SEG_OVERWRITE  1  /* out[s*w+j]  = count (fresh counter rows)   */
+/* optional launch-shape hint: lanes per segment (8, 16 or 32) in bits 8-15;
+ * 0 = automatic (fixed: from seg_bytes; CSR: 32 = one warp per segment)  */
+#define PP_SEG_LANES(g)   ((g) << 8)
 
 PP_API int         pp_abi_version(void);
 PP_API const char *pp_strerror(int code);

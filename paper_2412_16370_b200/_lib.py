@@ -13,7 +13,8 @@ import threading
 from .core import InputLengthError, KernelUnavailableError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpospopcnt_b200.so")
+# PP_LIB_PATH: load an alternative build (A/B experiments, scripts/)
+LIB_PATH = os.environ.get("PP_LIB_PATH") or os.path.join(HERE, "libpospopcnt_b200.so")
 
 PP_OK, PP_EWIDTH, PP_ELENGTH, PP_ECUDA, PP_EARG, PP_ENODEV = range(6)
 PP_SEG_ACCUMULATE, PP_SEG_OVERWRITE = 0, 1

@@ -125,6 +125,17 @@ int pp_count(const void *data, size_t nbytes, int width, unsigned long long *cou
   return count_device(data, nbytes, width, counters, static_cast<cudaStream_t>(stream), di);
 }
 
+// Lanes per segment: explicit hint in flags bits 8-15, else from the
+// (average) segment size: one warp per segment from 16 KiB up, 8 lanes
+// (4 segments per warp, 4x fewer transposes per segment) below 8 KiB.
+static int seg_lanes(int flags, unsigned long long avg_bytes) {
+  const int hint = (flags >> 8) & 0xFF;
+  if (hint == 8 || hint == 16 || hint == 32) return hint;
+  if (avg_bytes >= 16384) return 32;
+  if (avg_bytes >= 8192) return 16;
+  return 8;
+}
+
 static int seg_common(const pp::SegArgs &a, void *stream) {
   if (!width_ok(a.width)) return fail(PP_EWIDTH, "word width must be one of (8, 16, 32, 64), got %d", a.width);
   if (a.nseg == 0) return PP_OK;
@@ -149,6 +160,7 @@ int pp_count_segmented(const void *base, const unsigned long long *seg_off, size
   a.out = out;
   a.width = width;
   a.overwrite = (flags & PP_SEG_OVERWRITE) ? 1 : 0;
+  a.lanes_per_segment = seg_lanes(flags, 1ull << 20);  // unknown lengths: one warp each
   return seg_common(a, stream);
 }
 
@@ -165,6 +177,7 @@ int pp_count_fixed(const void *base, size_t seg_bytes, size_t nseg, int width,
   a.out = out;
   a.width = width;
   a.overwrite = (flags & PP_SEG_OVERWRITE) ? 1 : 0;
+  a.lanes_per_segment = seg_lanes(flags, seg_bytes);
   return seg_common(a, stream);
 }
 

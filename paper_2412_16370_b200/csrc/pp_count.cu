@@ -16,7 +16,7 @@
 // u64 frame[64] per CTA, and one u64 atomicAdd per (CTA, counter) after the
 // rotate-and-fold of flush_fw (accumulate.py:115-130).
 //
-// Segmented mode: pp_seg_kernel, one warp per segment.
+// Segmented mode: pp_seg_kernel<G>, G lanes per segment.
 #include "pp_device.cuh"
 #include "pp_internal.h"
 
@@ -35,6 +35,9 @@ constexpr int kLdgChunkVecs = kLdgThreads * 8;
 constexpr unsigned long long kLdgChunkBytes = kLdgChunkVecs * 16ull;
 
 constexpr int kSegThreads = 256;
+#ifndef PP_SEG_MIN_BLOCKS
+#define PP_SEG_MIN_BLOCKS 3  // <= 85 registers: 24 warps/SM of loads in flight
+#endif
 
 // Head/tail bytes (< 16 each) as one extra weight-1 plane pair, counted by
 // warp 0 of CTA 0.  Lane l < 16 takes head byte l, lane 16+l tail byte l.
@@ -192,18 +195,32 @@ __global__ void __launch_bounds__(kLdgThreads)
   fold_frame_to_counters(frame, a.counters, a.width, a.rot);
 }
 
-// One warp per segment; grid-stride over segments.  Each lane eats groups of
-// 8 coalesced 16-byte vectors; the segment's <16-byte head and tail become
-// one extra weight-1 plane.  Row s of out gets the rotated/folded counts.
-__global__ void __launch_bounds__(kSegThreads)
-    pp_seg_kernel(SegArgs a) {
-  const uint32_t lane = threadIdx.x & 31;
-  const unsigned long long gw = (blockIdx.x * (unsigned long long)kSegThreads + threadIdx.x) >> 5;
-  const unsigned long long nw = (gridDim.x * (unsigned long long)kSegThreads) >> 5;
-  const TC t = make_tc(lane);
-  const int w = a.width;
-  for (unsigned long long s = gw; s < a.nseg; s += nw) {
-    unsigned long long s0, s1;
+// Bytes [max(va, lo), min(va + 16, hi)) of the aligned 16-byte block at va,
+// zero elsewhere: the masked head / tail vector of a segment.  Exact-bounds
+// byte loads, so nothing outside the segment is ever read.
+__device__ __noinline__ uint4 load_partial(uintptr_t va, uintptr_t lo, uintptr_t hi) {
+  uint32_t q[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int b = 0; b < 16; ++b) {
+    const uintptr_t ad = va + b;
+    if (ad >= lo && ad < hi)
+      q[b >> 2] |= (uint32_t)__ldg(reinterpret_cast<const uint8_t *>(ad)) << (8 * (b & 3));
+  }
+  return make_uint4(q[0], q[1], q[2], q[3]);
+}
+
+// Geometry of segment s as "virtual vectors": the aligned 16-byte blocks
+// covering [p0, e).  Only vector 0 (head) and vector nvv-1 (tail) can be
+// partial; they are read with exact-bounds byte loads (load_partial).
+struct SegGeom {
+  uintptr_t p0, e, A;
+  unsigned long long nvv;
+  bool hp, tp;
+};
+
+__device__ __forceinline__ SegGeom seg_geom(const SegArgs &a, unsigned long long s) {
+  unsigned long long s0 = 0, s1 = 0;
+  if (s < a.nseg) {
     if (a.seg_off) {
       s0 = a.seg_off[s];
       s1 = a.seg_off[s + 1];
@@ -212,54 +229,124 @@ __global__ void __launch_bounds__(kSegThreads)
       s0 = s * a.seg_bytes;
       s1 = s0 + a.seg_bytes;
     }
-    const uint8_t *p0 = a.base + s0;
-    const unsigned long long n = s1 - s0;
-    const unsigned long long mis = (16u - ((uintptr_t)p0 & 15u)) & 15u;
-    const unsigned long long hb = mis < n ? mis : n;
-    const unsigned long long nv = (n - hb) >> 4;
-    const uint4 *body = reinterpret_cast<const uint4 *>(p0 + hb);
-    const uint32_t tb = (uint32_t)(n - hb - (nv << 4));
-    Counter c;
-    c.init();
-    for (unsigned long long g = 0; g < nv; g += 256) {
-      uint4 v[8];
-      if (g + 256 <= nv) {
+  }
+  SegGeom g;
+  g.p0 = reinterpret_cast<uintptr_t>(a.base) + s0;
+  g.e = g.p0 + (s1 - s0);
+  g.A = g.p0 & ~(uintptr_t)15;
+  g.nvv = (s1 > s0) ? (((g.e + 15) & ~(uintptr_t)15) - g.A) >> 4 : 0;
+  g.hp = (g.p0 & 15) != 0;
+  g.tp = (g.e & 15) != 0;
+  return g;
+}
+
+__device__ __forceinline__ bool seg_partial(const SegGeom &g, unsigned long long k) {
+  return (k == 0 && g.hp) || (k == g.nvv - 1 && g.tp);
+}
+
+// Row s of out <- the counts lane r of the segment's G-lane group holds
+// (frame bits G*f + r and 32 + G*f + r), rotated by rot = 8*(p0 mod 8) and
+// folded mod w exactly like flush_fw (accumulate.py:115-130).  All G lanes of
+// the group call this together (they share s).
+template <int G>
+__device__ __forceinline__ void write_row(const SegArgs &a, unsigned long long s,
+                                          uintptr_t p0, const GroupCounter<G> &c,
+                                          uint32_t lane) {
+  constexpr int S = 32 / G;
+  const int w = a.width;
+  const int r = (int)(lane % G);
+  const int rot = (int)(8u * (uint32_t)(p0 & 7u));
+  unsigned long long *row = a.out + s * (unsigned long long)w;
+  const bool ow = a.overwrite != 0;
+  if (w == 64) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = ldg_stream(body + g + j * 32 + lane);
+    for (int f = 0; f < S; ++f) {
+      const int pe = G * f + r;
+      unsigned long long *de = row + ((pe - rot) & 63), *dd = row + ((pe + 32 - rot) & 63);
+      *de = ow ? c.ce[f] : *de + c.ce[f];
+      *dd = ow ? c.co[f] : *dd + c.co[f];
+    }
+  } else if (G <= w) {
+    // lane r's positions G*f + r fall in w/G classes mod w; class of f is f % nc
+    const int nc = w / G;
+#pragma unroll
+    for (int cc = 0; cc < S; ++cc) {
+      if (cc < nc) {
+        unsigned long long tot = 0ull;
+#pragma unroll
+        for (int f = cc; f < S; ++f)
+          if (f % nc == cc) tot += c.ce[f] + c.co[f];
+        unsigned long long *d = row + ((G * cc + r - rot) & (w - 1));
+        *d = ow ? tot : *d + tot;
+      }
+    }
+  } else {
+    // G > w: all of lane r's positions are = r (mod w); lanes r, r^w, ... of
+    // the group share a class.
+    unsigned long long tot = 0ull;
+#pragma unroll
+    for (int f = 0; f < S; ++f) tot += c.ce[f] + c.co[f];
+    const unsigned gmask =
+        (G == 32) ? FULL : (((1u << G) - 1u) << (lane & ~(uint32_t)(G - 1)));
+    for (int m = w; m < G; m <<= 1) tot += __shfl_xor_sync(gmask, tot, m);
+    if (r < w) {
+      unsigned long long *d = row + ((r - rot) & (w - 1));
+      *d = ow ? tot : *d + tot;
+    }
+  }
+}
+
+// Segmented count fed by LDG, G lanes per segment (S = 32/G segments per
+// warp), grid-stride over groups of S segments.  Lane r of a segment eats
+// vectors r, r+G, ... in groups of 8 (G x 16 contiguous bytes per load
+// instruction per segment).  A TMA-fed variant (per-warp bulk-copy rings) was
+// 1.5x slower here: profiles/r1_segmented_ablation.md.
+template <int G>
+__global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
+    pp_seg_kernel(SegArgs a) {
+  constexpr int S = 32 / G;
+  const uint32_t lane = threadIdx.x & 31, r = lane % G, sl = lane / G;
+  const unsigned long long gw = (blockIdx.x * (unsigned long long)kSegThreads + threadIdx.x) >> 5;
+  const unsigned long long nw = (gridDim.x * (unsigned long long)kSegThreads) >> 5;
+  const TC t = make_tc(lane);
+  for (unsigned long long first = gw * S; first < a.nseg; first += nw * S) {
+    const unsigned long long s = first + sl;
+    const SegGeom g = seg_geom(a, s);
+    GroupCounter<G> c;
+    c.init();
+    // full (aligned, in-range) vectors are [kf0, kf1)
+    const unsigned long long kf0 = g.hp ? 1 : 0;
+    const unsigned long long kf1 = (g.tp && g.nvv) ? g.nvv - 1 : g.nvv;
+    const uint4 *vp = reinterpret_cast<const uint4 *>(g.A) + r;
+    auto load_round = [&](unsigned long long k0, uint4 (&v)[8]) {
+      if (k0 + r >= kf0 && k0 + r + 7 * G < kf1) {
+        // fast path: 8 full vectors, base pointer + immediate offsets
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = ldg_stream(vp + k0 + j * G);
       } else {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const unsigned long long idx = g + j * 32 + lane;
-          v[j] = idx < nv ? ldg_stream(body + idx) : make_uint4(0u, 0u, 0u, 0u);
+          const unsigned long long k = k0 + j * G + r;
+          v[j] = make_uint4(0u, 0u, 0u, 0u);
+          if (k < g.nvv) {
+            const uintptr_t va = g.A + 16 * k;
+            if (seg_partial(g, k))
+              v[j] = load_partial(va, g.p0, g.e);
+            else
+              v[j] = ldg_stream(reinterpret_cast<const uint4 *>(va));
+          }
         }
       }
+    };
+    // (a software-pipelined variant that keeps the next round in flight was
+    // no faster: profiles/r1_segmented_ablation.md)
+    for (unsigned long long k0 = 0; __any_sync(FULL, k0 < g.nvv); k0 += 8 * G) {
+      uint4 v[8];
+      load_round(k0, v);
       c.eat8(v, t);
     }
-    if (hb | tb) count_edges(c, p0, (uint32_t)hb, (const uint8_t *)(body + nv), tb, lane, t);
     c.finish(t);
-    const int rot = (int)frame_shift(p0);
-    unsigned long long *row = a.out + s * (unsigned long long)w;
-    if (w == 64) {
-      const int j0 = ((int)lane - rot) & 63, j1 = ((int)lane + 32 - rot) & 63;
-      if (a.overwrite) {
-        row[j0] = c.ce;
-        row[j1] = c.co;
-      } else {
-        row[j0] += c.ce;
-        row[j1] += c.co;
-      }
-    } else {
-      unsigned long long tot = c.ce + c.co;
-      if (w <= 16) tot += __shfl_xor_sync(FULL, tot, 16);
-      if (w <= 8) tot += __shfl_xor_sync(FULL, tot, 8);
-      if ((int)lane < w) {
-        const int j = ((int)lane - rot) & (w - 1);
-        if (a.overwrite)
-          row[j] = tot;
-        else
-          row[j] += tot;
-      }
-    }
+    if (s < a.nseg) write_row<G>(a, s, g.p0, c, lane);
   }
 }
 
@@ -298,8 +385,8 @@ cudaError_t device_info(int dev, DevInfo *out) {
     if ((e = cudaFuncSetAttribute(pp_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kTmaSmemBytes)))
       return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.seg_blocks_per_sm, pp_seg_kernel,
-                                                           kSegThreads, 0)))
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.seg_blocks_per_sm,
+                                                           pp_seg_kernel<8>, kSegThreads, 0)))
       return e;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.ldg_blocks_per_sm,
                                                            pp_count_ldg_kernel, kLdgThreads, 0)))
@@ -340,10 +427,16 @@ cudaError_t launch_readonly(const CountArgs &a, unsigned long long *sink, const 
 
 cudaError_t launch_segmented(const SegArgs &a, const DevInfo &di, cudaStream_t st) {
   if (a.nseg == 0) return cudaSuccess;
-  const unsigned long long warps_per_block = kSegThreads / 32;
-  const unsigned long long need = (a.nseg + warps_per_block - 1) / warps_per_block;
+  const int G = a.lanes_per_segment;
+  const unsigned long long segs_per_block = (kSegThreads / 32) * (32 / G);
+  const unsigned long long need = (a.nseg + segs_per_block - 1) / segs_per_block;
   const unsigned g = grid_for(need, (unsigned long long)di.num_sms * di.seg_blocks_per_sm);
-  pp_seg_kernel<<<g, kSegThreads, 0, st>>>(a);
+  if (G == 8)
+    pp_seg_kernel<8><<<g, kSegThreads, 0, st>>>(a);
+  else if (G == 16)
+    pp_seg_kernel<16><<<g, kSegThreads, 0, st>>>(a);
+  else
+    pp_seg_kernel<32><<<g, kSegThreads, 0, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -199,6 +199,106 @@ struct Counter {
   }
 };
 
+// Segment-parallel variant: G lanes share one segment, so a warp carries
+// S = 32/G independent segments.  Each transpose stage swaps one bit of the
+// lane index with the same bit of the bit index, and the stages commute, so
+// running only the stages j < G transposes inside each G-lane group: lane r
+// of a group then holds, in G-bit field f, the group's bits of position
+// G*f + r, and one masked __popc per field gives its segment's count.
+template <int G>
+__device__ __forceinline__ uint32_t gtranspose(uint32_t x, const TC &t) {
+  uint32_t y;
+  if (G > 16) {
+    y = __shfl_xor_sync(FULL, x, 16);
+    x = __byte_perm(x, y, t.sel16);
+  }
+  if (G > 8) {
+    y = __shfl_xor_sync(FULL, x, 8);
+    x = __byte_perm(x, y, t.sel8);
+  }
+  y = __shfl_xor_sync(FULL, x, 4);
+  y = __funnelshift_r(y, y, t.rot4);
+  x = (x & t.keep4) | (y & ~t.keep4);
+  y = __shfl_xor_sync(FULL, x, 2);
+  y = __funnelshift_r(y, y, t.rot2);
+  x = (x & t.keep2) | (y & ~t.keep2);
+  y = __shfl_xor_sync(FULL, x, 1);
+  y = __funnelshift_r(y, y, t.rot1);
+  x = (x & t.keep1) | (y & ~t.keep1);
+  return x;
+}
+
+template <int G>
+struct GroupCounter {
+  static_assert(G == 8 || G == 16 || G == 32, "lanes per segment");
+  static constexpr int S = 32 / G;  // positions per lane per tree
+  Planes l1e, l1o, l2e, l2o;
+  uint32_t l2n;
+  // lane r of a segment's group: frame bits G*f + r (e) and 32 + G*f + r (o)
+  unsigned long long ce[S], co[S];
+
+  __device__ __forceinline__ void init() {
+    l1e = l1o = l2e = l2o = Planes{0u, 0u, 0u, 0u};
+    l2n = 0;
+#pragma unroll
+    for (int f = 0; f < S; ++f) ce[f] = co[f] = 0ull;
+  }
+
+  static __device__ __forceinline__ uint32_t field_popc(uint32_t x, int f) {
+    if (G == 32) return __popc(x);
+    return __popc(x & ((G == 16 ? 0xFFFFu : 0xFFu) << (f * G)));
+  }
+
+  // Count the first np planes (weights 1,2,4,8 << shift) of both trees.
+  __device__ __forceinline__ void count_planes(const Planes &pe, const Planes &po, int np,
+                                               int shift, const TC &t) {
+    uint32_t se[S], so[S];
+#pragma unroll
+    for (int f = 0; f < S; ++f) se[f] = so[f] = 0u;
+    const uint32_t ve[4] = {pe.p1, pe.p2, pe.p4, pe.p8};
+    const uint32_t vo[4] = {po.p1, po.p2, po.p4, po.p8};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < np) {  // np is warp-uniform
+        const uint32_t te = gtranspose<G>(ve[k], t), to = gtranspose<G>(vo[k], t);
+#pragma unroll
+        for (int f = 0; f < S; ++f) {
+          se[f] += field_popc(te, f) << k;
+          so[f] += field_popc(to, f) << k;
+        }
+      }
+    }
+#pragma unroll
+    for (int f = 0; f < S; ++f) {
+      ce[f] += (unsigned long long)se[f] << shift;
+      co[f] += (unsigned long long)so[f] << shift;
+    }
+  }
+
+  __device__ __forceinline__ void eat8(const uint4 (&v)[8], const TC &t) {
+    uint32_t ev[16], od[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      ev[2 * i] = v[i].x;
+      ev[2 * i + 1] = v[i].z;
+      od[2 * i] = v[i].y;
+      od[2 * i + 1] = v[i].w;
+    }
+    inc4(l2e, csa16_4(l1e, ev));
+    inc4(l2o, csa16_4(l1o, od));
+    if (++l2n == 15) {
+      count_planes(l2e, l2o, 4, 4, t);
+      l2e = l2o = Planes{0u, 0u, 0u, 0u};
+      l2n = 0;
+    }
+  }
+
+  __device__ __forceinline__ void finish(const TC &t) {
+    count_planes(l1e, l1o, 4, 0, t);
+    if (l2n) count_planes(l2e, l2o, l2n >= 8 ? 4 : l2n >= 4 ? 3 : l2n >= 2 ? 2 : 1, 4, t);
+  }
+};
+
 // Frame position (mod 64) of bit 0 of the byte at address a.
 __device__ __forceinline__ uint32_t frame_shift(const void *a) {
   return 8u * (uint32_t)(reinterpret_cast<uintptr_t>(a) & 7u);

@@ -30,6 +30,7 @@ struct SegArgs {
   unsigned long long *out;
   int width;
   int overwrite;
+  int lanes_per_segment;  // G in {8, 16, 32}
 };
 
 enum class LoadPath : int { kTma = 0, kLdg = 1 };

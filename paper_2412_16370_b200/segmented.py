@@ -39,14 +39,17 @@ def _out_tensor(out, nseg, width, device):
     return out, False
 
 
-def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validate=True):
+def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validate=True,
+                        lanes=None):
     """Positional counts of many arrays in one launch.
 
     ``offsets``: nseg+1 non-decreasing byte offsets into the view (host
     sequence / numpy array, or a CUDA int64 tensor).  ``out``: CUDA
     (nseg, width) int64 tensor accumulated into (or overwritten when
     ``accumulate=False``); allocated zeroed when None.  Returns ``out``.
-    Asynchronous on the current stream.
+    Asynchronous on the current stream.  ``lanes`` (8, 16 or 32) forces the
+    lanes-per-segment launch shape; by default it follows the mean segment
+    length when the offsets are on the host.
     """
     import torch
     check_width(width)
@@ -73,12 +76,16 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
             if (d % step).any():
                 raise InputLengthError(f"a segment is not a multiple of the {step}-byte word size")
         offs = torch.as_tensor(offs_np, device=dev)
+        if lanes is None and offs_np.size > 1:
+            mean = (int(offs_np[-1]) - int(offs_np[0])) // (offs_np.size - 1)
+            lanes = 32 if mean >= 16384 else 16 if mean >= 8192 else 8
     nseg = offs.numel() - 1
     out, fresh = _out_tensor(out, max(nseg, 0), width, dev)
     if nseg <= 0:
         return out
     lib = _lib.load()
     flags = _lib.PP_SEG_ACCUMULATE if (accumulate and not fresh) else _lib.PP_SEG_OVERWRITE
+    flags |= _lanes_flag(lanes)
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream(dev).cuda_stream
         base_ptr = view.base.data_ptr() + view.offset
@@ -89,7 +96,15 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
     return out
 
 
-def pospopcnt_fixed(data, seg_bytes, width, out=None, accumulate=True):
+def _lanes_flag(lanes):
+    if lanes is None:
+        return 0
+    if lanes not in (8, 16, 32):
+        raise ValueError("lanes must be 8, 16 or 32")
+    return lanes << 8
+
+
+def pospopcnt_fixed(data, seg_bytes, width, out=None, accumulate=True, lanes=None):
     """Equal-size segments: segment s = bytes [s*seg_bytes, (s+1)*seg_bytes) of the view.
 
     A trailing partial segment is not counted (nseg = nbytes // seg_bytes).
@@ -109,6 +124,7 @@ def pospopcnt_fixed(data, seg_bytes, width, out=None, accumulate=True):
         return out
     lib = _lib.load()
     flags = _lib.PP_SEG_ACCUMULATE if (accumulate and not fresh) else _lib.PP_SEG_OVERWRITE
+    flags |= _lanes_flag(lanes)
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream(dev).cuda_stream
         _lib.check(lib.pp_count_fixed(view.base.data_ptr() + view.offset, seg_bytes, nseg,

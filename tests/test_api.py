@@ -81,6 +81,47 @@ def test_inputview_nbytes_of_arrays_and_tensors():
     assert not InputView.of(torch.zeros(4, dtype=torch.uint8)).on_device
 
 
+def test_foreign_view_is_adopted():
+    """The reference passes its own InputView to kernel.run (kernels.py:333)."""
+    from dataclasses import dataclass
+
+    @dataclass(frozen=True)
+    class RefView:  # shape of pospopcnt.core.InputView
+        base: object
+        offset: int
+        nbytes: int
+
+    v = InputView.of(RefView(b"abcdefgh", 2, 4))
+    assert isinstance(v, InputView) and bytes(v.mv()) == b"cdef"
+
+
+def test_reference_package_drives_b200_kernel_object():
+    """Load the unmodified reference (build container only) and hand it our
+    kernel object: validation, dispatch and error classes are the reference's."""
+    import importlib.util
+    import sys
+    src = "/root/reference/pkg/src/pospopcnt"
+    if not os.path.exists(src):
+        pytest.skip("reference not mounted here")
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/pospopcnt_ref_numba_cache")
+    spec = importlib.util.spec_from_file_location(
+        "pospopcnt_ref_t", os.path.join(src, "__init__.py"), submodule_search_locations=[src])
+    ref = importlib.util.module_from_spec(spec)
+    sys.modules["pospopcnt_ref_t"] = ref
+    old = sys.dont_write_bytecode
+    sys.dont_write_bytecode = True
+    try:
+        spec.loader.exec_module(ref)
+    finally:
+        sys.dont_write_bytecode = old
+    k = kernels.B200Kernel()
+    with pytest.raises(ref.InputLengthError):
+        ref.pospopcnt(b"\x00" * 7, 64, kernel=k)
+    if not k.available():
+        with pytest.raises(ref.KernelUnavailableError):
+            ref.pospopcnt(b"\x01\x80", 16, kernel=k)
+
+
 def test_registry_contract(monkeypatch):
     """kernels.py:276-312 semantics with the one B200 kernel."""
     pairs = pp.list_kernels()

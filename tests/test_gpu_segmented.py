@@ -49,11 +49,18 @@ def test_c1_exhaustive_sweep_via_segments(cuda, oracle):
         offs[-1] = len(cases) * slot
         buf = torch.from_numpy(host).cuda()
         doffs = torch.from_numpy(offs).cuda()
-        out = torch.zeros((3 * len(cases), w), dtype=torch.int64, device="cuda")
-        rc = lib.pp_count_segmented(buf.data_ptr(), doffs.data_ptr(), 3 * len(cases), w,
-                                    out.data_ptr(), _lib.PP_SEG_OVERWRITE, None)
-        _lib.check(rc)
-        got = out.cpu().numpy().view(np.uint64)[real_rows]
+        got = None
+        for lanes, path in ((32, 0), (16, 0), (8, 0)):
+            # every launch shape must agree
+            out = torch.zeros((3 * len(cases), w), dtype=torch.int64, device="cuda")
+            rc = lib.pp_count_segmented(buf.data_ptr(), doffs.data_ptr(), 3 * len(cases), w,
+                                        out.data_ptr(),
+                                        _lib.PP_SEG_OVERWRITE | (lanes << 8) | path, None)
+            _lib.check(rc)
+            rows = out.cpu().numpy().view(np.uint64)[real_rows]
+            if got is not None:
+                assert np.array_equal(rows, got), (w, lanes)
+            got = rows
         # oracle: the same views of the same bytes
         st = np.array([a for a, _ in exp_offs], dtype=np.uint64)
         en = np.array([b for _, b in exp_offs], dtype=np.uint64)
@@ -67,7 +74,8 @@ def test_c1_exhaustive_sweep_via_segments(cuda, oracle):
                 dig["sha256_u64_rows"], w
 
 
-def test_ragged_random_segments_poison(cuda, oracle, rng):
+@pytest.mark.parametrize("lanes", (None, 8, 16, 32))
+def test_ragged_random_segments_poison(cuda, oracle, rng, lanes):
     torch, pp = cuda
     for w in (8, 16, 32, 64):
         step = w // 8
@@ -79,30 +87,31 @@ def test_ragged_random_segments_poison(cuda, oracle, rng):
         host = np.frombuffer(rng.randbytes(int(offs[-1]) + base + 11), np.uint8).copy()
         buf = torch.from_numpy(host).cuda()
         view = pp.InputView(buf, base, int(offs[-1]))
-        out = pp.pospopcnt_segmented(view, offs, w)
+        out = pp.pospopcnt_segmented(view, offs, w, lanes=lanes)
         want = oracle.segments(host, (offs + base).astype(np.uint64), w)
         assert np.array_equal(out.cpu().numpy().view(np.uint64), want), w
         # accumulate semantics
-        pp.pospopcnt_segmented(view, offs, w, out=out)
+        pp.pospopcnt_segmented(view, offs, w, out=out, lanes=lanes)
         assert np.array_equal(out.cpu().numpy().view(np.uint64), 2 * want), w
-        pp.pospopcnt_segmented(view, offs, w, out=out, accumulate=False)
+        pp.pospopcnt_segmented(view, offs, w, out=out, accumulate=False, lanes=lanes)
         assert np.array_equal(out.cpu().numpy().view(np.uint64), want), w
 
 
-def test_config_c4_segmented_batch(cuda, oracle):
+@pytest.mark.parametrize("lanes", (8, 32))
+def test_config_c4_segmented_batch(cuda, oracle, lanes):
     """262,144 independent 4 KiB arrays of Bernoulli(0.01) bits, w=64."""
     torch, pp = cuda
     from paper_2412_16370_b200 import gen
     nseg, seg = 262_144, 4096
     buf = gen.generate("bernoulli", nseg * seg, 0xC4 + 1, q=655)
-    out = pp.pospopcnt_fixed(buf, seg, 64)
+    out = pp.pospopcnt_fixed(buf, seg, 64, lanes=lanes)
     got = out.cpu().numpy().view(np.uint64)
     host = buf.cpu().numpy()
     offs = np.arange(nseg + 1, dtype=np.uint64) * seg
     want = oracle.segments(host, offs, 64)
     assert np.array_equal(got, want)
     # the fixed and CSR entry points agree
-    out2 = pp.pospopcnt_segmented(buf, offs.astype(np.int64), 64)
+    out2 = pp.pospopcnt_segmented(buf, offs.astype(np.int64), 64, lanes=lanes)
     assert np.array_equal(out2.cpu().numpy().view(np.uint64), want)
 
 
