@@ -107,6 +107,18 @@ PP_API int pp_count_fixed(const void *base, size_t seg_bytes, size_t nseg, int w
                    unsigned long long *out, int flags, void *stream);
 
 /*
+ * pp_count_frame — one pass for every word width:
+ * frame64[i] += #{set bits b of bytes at address A : 8*(A mod 8) + b == i}
+ * over the device bytes [data, data+nbytes) (any length, any alignment).
+ * Width w, for any w with nbytes % (w/8) == 0, is then the fold of
+ * flush_fw (accumulate.py:115-130):
+ *   C_w[j] = sum_{i = j mod w} frame64[(i + rot) mod 64],  rot = 8*(data mod 8)
+ * which is the width-refinement identity of pkg/tests/test_core.py:66-72.
+ */
+PP_API int pp_count_frame(const void *data, size_t nbytes, unsigned long long *frame64,
+                          void *stream);
+
+/*
  * pp_readonly_sum — the paper's "roofline" dummy kernel:
  * streams nbytes through exactly the load path of pp_count and XORs them into
  * *sink (DEVICE, 1 uint64).  Measurement only.

@@ -30,6 +30,7 @@ SIGNATURES = {
     "pp_device_info": (_int, [_int, _vp, _vp, _vp]),
     "pp_count": (_int, [_vp, _sz, _int, _vp, _vp]),
     "pp_count_host": (_int, [_vp, _sz, _int, _vp]),
+    "pp_count_frame": (_int, [_vp, _sz, _vp, _vp]),
     "pp_count_segmented": (_int, [_vp, _vp, _sz, _int, _vp, _int, _vp]),
     "pp_count_fixed": (_int, [_vp, _sz, _sz, _int, _vp, _int, _vp]),
     "pp_readonly_sum": (_int, [_vp, _sz, _vp, _vp]),

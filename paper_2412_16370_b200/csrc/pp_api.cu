@@ -69,12 +69,13 @@ int check_device_ptr(const void *p, const char *what) {
 }
 
 int count_device(const void *data, size_t nbytes, int width, unsigned long long *counters,
-                 cudaStream_t st, const pp::DevInfo &di) {
+                 cudaStream_t st, const pp::DevInfo &di, bool raw_frame = false) {
   pp::CountArgs a{};
   const pp::LoadPath path = load_path();
   pp::split_range(static_cast<const uint8_t *>(data), nbytes, pp::count_chunk_bytes(path), &a);
   a.counters = counters;
   a.width = width;
+  if (raw_frame) a.rot = 0;  // frame[i] as is: bit i mod 8 of bytes at address = i/8 mod 8
   cudaError_t e = pp::launch_count(a, path, di, st);
   if (e != cudaSuccess) return cuda_fail(e, "pp_count launch");
   return PP_OK;
@@ -123,6 +124,17 @@ int pp_count(const void *data, size_t nbytes, int width, unsigned long long *cou
   pp::DevInfo di;
   if ((rc = current_devinfo(&di))) return rc;
   return count_device(data, nbytes, width, counters, static_cast<cudaStream_t>(stream), di);
+}
+
+int pp_count_frame(const void *data, size_t nbytes, unsigned long long *frame64,
+                   void *stream) {
+  int rc;
+  if ((rc = check_device_ptr(frame64, "frame64"))) return rc;
+  if (nbytes == 0) return PP_OK;
+  if ((rc = check_device_ptr(data, "data"))) return rc;
+  pp::DevInfo di;
+  if ((rc = current_devinfo(&di))) return rc;
+  return count_device(data, nbytes, 64, frame64, static_cast<cudaStream_t>(stream), di, true);
 }
 
 // Lanes per segment: explicit hint in flags bits 8-15, else from the

@@ -259,6 +259,53 @@ def pospopcnt(data, width, counters=None, kernel=None):
     return kernel.run(view, width, counters)
 
 
+def fold_frame(frame, w, rot):
+    """C_w[j] = sum_{i = j mod w} frame[(i + rot) mod 64]  (flush_fw, accumulate.py:115-130)."""
+    return [sum(int(frame[(i + rot) % W_MAX]) for i in range(j, W_MAX, w)) for j in range(w)]
+
+
+def pospopcnt_all_widths(data, widths=None):
+    """Every word width from ONE pass over the data.
+
+    Counts the 64-position address frame once on the GPU (pp_count_frame)
+    and folds it for each w in ``widths`` (default: every width the length
+    is word-complete for) — the width-refinement identity
+    C_w[j] = C_2w[j] + C_2w[j+w] (pkg/tests/test_core.py:66-72).
+    Returns {w: list of w counters}.  Host data is copied to the current
+    CUDA device once.
+    """
+    import torch
+    view = InputView.of(data)
+    if widths is None:
+        widths = [w for w in (8, 16, 32, 64) if view.nbytes % (w // 8) == 0]
+    for w in widths:
+        check_width(w)
+        view.check_complete(w)
+    lib = _lib.load()
+    if view.on_device:
+        base, off = view.base, view.offset
+    else:
+        ptr, keep = _host_u8(view.base, view.offset, view.nbytes)
+        host = np.ctypeslib.as_array((ctypes.c_uint8 * view.nbytes).from_address(ptr)) \
+            if view.nbytes else np.zeros(0, np.uint8)
+        base, off = torch.from_numpy(host.copy()).cuda(), 0
+        del keep
+    if not base.is_contiguous():
+        raise ValueError("input tensor must be contiguous")
+    dev = base.device
+    frame = np.zeros(W_MAX, dtype=np.uint64)
+    ptr = base.data_ptr() + off
+    if view.nbytes:
+        with torch.cuda.device(dev):
+            scratch = _device_scratch(dev)
+            scratch.zero_()
+            stream = torch.cuda.current_stream(dev).cuda_stream
+            _lib.check(lib.pp_count_frame(ptr, view.nbytes, scratch.data_ptr(), stream))
+            frame = scratch.cpu().numpy().view(np.uint64)
+    rot = 8 * (ptr % 8)
+    return {w: fold_frame(frame, w, rot) for w in widths}
+
+
 def count_device(ptr, nbytes, width, counters_ptr, stream=0):
     """Raw device-pointer entry (pp_count), for callers managing their own memory."""
     lib = _lib.load()

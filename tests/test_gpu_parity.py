@@ -284,3 +284,43 @@ def test_concurrent_threads_distinct_counters(cuda, rng):
         t.join()
     assert not errors and all(results) and len(results) == 6
     assert want == oracle_bits(data[:4096], 16)
+
+
+def test_all_widths_from_one_frame_pass(cuda, oracle, rng):
+    """one pass, every width, any alignment (incl. words
+    straddling 16-byte vectors)."""
+    torch, pp = cuda
+    host = np.frombuffer(rng.randbytes((1 << 20) + 64), np.uint8)
+    buf = torch.from_numpy(host.copy()).cuda()
+    for off, n in ((0, 1 << 20), (3, (1 << 20) - 8), (5, 1000), (7, 6), (1, 3), (0, 0)):
+        got = pp.pospopcnt_all_widths(pp.InputView(buf, off, n))
+        for w, cnt in got.items():
+            assert cnt == oracle.hs512(host, off, n, w), (off, n, w)
+        assert set(got) == {w for w in (8, 16, 32, 64) if n % (w // 8) == 0}
+    assert pp.pospopcnt_all_widths(host[3:3 + 4096].tobytes(), widths=(16,)) == \
+        {16: oracle.hs512(host, 3, 4096, 16)}
+
+
+def test_cuda_graph_capture_and_replay(cuda, oracle, rng):
+    """pp_count is capture-safe: a captured count replays on new data."""
+    torch, pp = cuda
+    host = np.frombuffer(rng.randbytes(3 << 20), np.uint8)
+    buf = torch.from_numpy(host.copy()).cuda()
+    cnt = torch.zeros(16, dtype=torch.int64, device="cuda")
+    pp.pospopcnt(buf, 16, counters=cnt)  # warm (device info, attributes)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        pp.pospopcnt(pp.InputView(buf, 5, 2 << 20), 16, counters=cnt)
+    cnt.zero_()
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    want = oracle.hs512(host, 5, 2 << 20, 16)
+    assert [int(x) for x in cnt.cpu()] == [2 * v for v in want]
+    host2 = np.frombuffer(rng.randbytes(3 << 20), np.uint8)
+    buf.copy_(torch.from_numpy(host2.copy()))
+    cnt.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert [int(x) for x in cnt.cpu()] == oracle.hs512(host2, 5, 2 << 20, 16)
