@@ -41,15 +41,25 @@ GIB = 1 << 30
 MIB = 1 << 20
 
 CONFIGS = {
-    # name: (generator, width, bytes per GPU, description)
+    # name: (generator, width, bytes per GPU (weak) or in total (strong), description)
     "c1": ("uniform", 16, 2 * MIB, "w=16, 2 MiB, Bernoulli(0.5), aligned"),
     "c2": ("uniform", 8, GIB, "w=8, 1 GiB, Bernoulli(0.5)"),
     "c3": ("onehot32", 32, 4 * GIB, "w=32 one-hot, 4 GiB, bounded Zipf(1.1) over 32 bits"),
     "c4": ("bernoulli", 64, 64 * MIB, "w=64, 64 MiB at byte offset 3, Bernoulli(0.01)"),
     "c4seg": ("bernoulli", 64, GIB, "w=64, 262,144 segments x 4 KiB, Bernoulli(0.01)"),
-    "c5": ("blocks", 16, 8 * GIB, "w=16, 8 GiB shard per GPU of the 64 GiB array, "
-                                  "Bernoulli(p) with p ~ U[0,1] per 1 MiB block"),
+    "c5": ("blocks", 16, 64 * GIB, "w=16, 64 GiB array sharded over the GPUs (8 GiB per GPU "
+                                   "at N=8), Bernoulli(p) with p ~ U[0,1] per 1 MiB block"),
 }
+STRONG = {"c5"}  # total work fixed as N grows; every other config is per-GPU (weak)
+
+
+def golden_total(name):
+    """The reference's own counters for a full config (tests/golden/golden.json)."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
+            return json.load(f)["digests"][name]["expected"]
+    except Exception:  # noqa: BLE001
+        return None
 
 
 def load_peaks():
@@ -62,15 +72,18 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def load_traffic(kernel_key):
-    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+def load_traffic(kernel_key, input_bytes):
+    """(dram bytes per launch, dram bytes per input byte) of the dominant kernel
+    from the committed ncu capture; the absolute figure only when the capture
+    counted a launch of the same input size as this one."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d.get(kernel_key)
+            d = json.load(f)[kernel_key]
+        ratio = d["bytes"] / d["input_bytes"]
+        return (d["bytes"] if d["input_bytes"] == input_bytes else None), round(ratio, 5)
     except Exception:  # noqa: BLE001
-        return None
+        return None, None
 
 
 class ClockSampler:
@@ -96,7 +109,18 @@ class ClockSampler:
             import pynvml
             pynvml.nvmlInit()
             self.nvml = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.h = None
+            try:  # CUDA ordinal -> NVML handle via the PCI bus id (CUDA_VISIBLE_DEVICES-safe)
+                import torch
+                pr = torch.cuda.get_device_properties(self.index)
+                dom, bus, devn = (int(pr.pci_domain_id), int(pr.pci_bus_id),
+                                  int(pr.pci_device_id))
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(
+                    f"{dom:08X}:{bus:02X}:{devn:02X}.0")
+            except Exception:  # noqa: BLE001
+                self.h = None
+            if self.h is None:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
         except Exception:  # noqa: BLE001
             self.nvml = None
@@ -194,6 +218,7 @@ def run_reference(args):
     kind, w, nbytes, desc = CONFIGS[cfg]
     if cfg == "c4seg":
         kind, w, nbytes = "bernoulli", 64, GIB
+    nbytes = min(nbytes, GIB)  # bounded sample of the workload (the metric is a rate)
     if kind == "uniform":
         host = O.gen_uniform(nbytes, 0xC2 if cfg == "c2" else 0xC1)
     elif kind == "onehot32":
@@ -258,10 +283,18 @@ def main_gpu(args):
         w = args.width
     seed = {"c1": 0xC1, "c2": 0xC2, "c3": 0xC3, "c4": 0xC4, "c4seg": 0xC4 + 1, "c5": 0xC5}[cfg]
     offset = 3 if cfg == "c4" else 0
-    alloc = nbytes + (64 if cfg == "c4" else 0)
     word_unit = 4 if kind == "onehot32" else 8
-    buf = gen.generate(kind, alloc, seed, device=dev,
-                       word_offset=rank * alloc // word_unit, q=655)
+    strong = cfg in STRONG
+    if strong:
+        # contiguous shard of the fixed-size array, cut at 64-byte multiples
+        from paper_2412_16370_b200.dist import shard_range
+        lo, hi = shard_range(nbytes, world, rank)
+        nbytes = hi - lo
+        alloc, first_word = nbytes, lo // word_unit
+    else:
+        alloc = nbytes + (64 if cfg == "c4" else 0)
+        first_word = rank * alloc // word_unit
+    buf = gen.generate(kind, alloc, seed, device=dev, word_offset=first_word, q=655)
     view_ptr = buf.data_ptr() + offset
     torch.cuda.synchronize()
 
@@ -320,12 +353,25 @@ def main_gpu(args):
         tt = torch.tensor([t_ms, k_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms, k_ms = tt.tolist()
-    per_step_bytes = nbytes
-    value = world * per_step_bytes * args.steps / (t_ms / 1e3) / 1e9
+    per_step_bytes = nbytes  # this rank's bytes per step
+    job_bytes = per_step_bytes
+    if world > 1:
+        jb = torch.tensor([per_step_bytes], dtype=torch.int64, device=dev)
+        dist.all_reduce(jb)
+        job_bytes = int(jb.item())
+    value = job_bytes * args.steps / (t_ms / 1e3) / 1e9
 
-    # exactness vs the oracle (full array, C2 and C1 and c4)
+    # exactness: C5 against the reference's own 64 GiB total (golden file),
+    # the others against the CPU oracle on this rank's shard
     exact = None
-    if args.check and cfg in ("c1", "c2", "c3", "c4", "c5") and rank == 0:
+    if args.check and cfg == "c5" and rank == 0:
+        want = golden_total("c5_w16_64gib_total")
+        src = glob if world > 1 else counters
+        got = src.cpu().numpy().view(np.uint64)[:w]
+        total = args.warmup + args.steps
+        exact = None if want is None else bool(
+            all(int(g) == total * x for g, x in zip(got, want)))
+    elif args.check and cfg in ("c1", "c2", "c3", "c4") and rank == 0:
         from oracle import oracle as O
         host = buf.cpu().numpy()
         want = O.hs512(host, offset, nbytes, w, threads=host_threads())
@@ -350,11 +396,12 @@ def main_gpu(args):
     peak, peak_src = load_peaks()
     achieved = per_step_bytes / (k_ms / 1e3) / 1e9
     kernel_key = "pp_seg_kernel" if seg_out is not None else "pp_tma_kernel<true>"
-    traffic = load_traffic(kernel_key)
+    traffic, traffic_ratio = load_traffic(kernel_key, per_step_bytes)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
                 "kernel": kernel_key, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": per_step_bytes,
+                "traffic_per_input_byte_ncu": traffic_ratio,
                 "readonly_roofline_gbs": round(ro_gbs, 1)}
     if seg_out is not None:
         seg_bytes_out = (nbytes // 4096) * w * 8
@@ -364,7 +411,7 @@ def main_gpu(args):
 
     # e2e through the public API from pinned host memory
     e2e = None
-    if args.e2e and seg_out is None:
+    if args.e2e and seg_out is None and nbytes <= 4 * GIB:
         pinned = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
         pinned.copy_(buf[offset:offset + nbytes])
         torch.cuda.synchronize()
@@ -404,15 +451,20 @@ def main_gpu(args):
             "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(t_ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8" if w == 8 else f"u{w}",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None,
+            "dtype": "u8" if w == 8 else f"u{w}",
             "data": "synthetic: seeded splitmix64 generators, generated in place in HBM",
             "config": {"workload": desc, "word_width": w,
                        "bytes_per_gpu_per_step": per_step_bytes,
+                       "bytes_per_step_all_gpus": job_bytes,
                        "parallelism": f"dp{world} (contiguous shards, NCCL allreduce of "
                                       f"{w} counters per step)" if world > 1 else "single GPU",
                        "l2": "input >> 126 MB L2, no flush needed" if nbytes > 256 * MIB
                              else "input fits L2 (reported, not judged vs HBM)"},
             "hbm_frac": round(value / world / peak, 4),
+            "exact_reference": "C5: reference numba total of the 64 GiB array (golden.json)"
+                               if cfg == "c5" else "CPU oracle (C port of NumbaKernel.run) "
+                                                   "on rank 0's shard",
             "words_per_s": round(value * 1e9 / (w // 8)),
             "roofline": roofline,
             "cpu_baseline": cpu,

@@ -80,7 +80,8 @@ def main(rep, launches, prefix):
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(ur, 1)
         uw = units[hdr.index("dram__bytes_write.sum")]
         scw = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(uw, 1)
-        traffic.setdefault(name, int(float(rd) * scale + float(wr) * scw))
+        traffic.setdefault(name, {"bytes": int(float(rd) * scale + float(wr) * scw),
+                                  "input_bytes": 1 << 30})
     with open(prefix + "_ncu_summary.md", "w") as f:
         f.write("\n".join(out) + "\n")
     # launch list: keep the per-launch rows
