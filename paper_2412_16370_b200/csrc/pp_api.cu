@@ -4,8 +4,13 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "../../include/pospopcnt_b200.h"
 #include "pp_internal.h"
@@ -209,18 +214,109 @@ int pp_readonly_sum(const void *data, size_t nbytes, unsigned long long *sink, v
 }
 
 // ---------------------------------------------------------------- host path
-// Per-thread staging context: NBUF device buffers, a copy stream and a count
-// stream.  Chunk i is copied H2D into buffer i % NBUF on the copy stream while
-// chunk i-1 is counted on the count stream; the chunks are word-complete
-// (CHUNK is a multiple of 64), so their counts simply add.
+// Host-buffer path.  Per-thread staging context: NBUF device buffers, a copy
+// stream and a count stream.  Chunk i is copied H2D into device buffer
+// i % NBUF on the copy stream while chunk i-1 is counted on the count stream;
+// chunks are word-complete (CHUNK is a multiple of 64), so their counts simply
+// add.  Pinned sources are DMA'd directly.  Pageable sources
+// (bytes / bytearray / numpy: the reference's own inputs) would be staged by
+// the driver on one thread at ~15 GB/s, so they go through NBUF pinned
+// buffers filled by a persistent copy pool, overlapped with the DMA of the
+// previous chunk and the count of the one before.
 namespace {
 constexpr int kNbuf = 3;
 constexpr size_t kChunk = 32ull << 20;
+
+// Parallel memcpy on a persistent pool; the calling thread works too.
+class CopyPool {
+ public:
+  static CopyPool &get() {
+    static CopyPool *pool = new CopyPool();  // intentionally leaked (process lifetime)
+    return *pool;
+  }
+  void copy(void *dst, const void *src, size_t n) {
+    if (workers_.empty() || n < (4u << 20)) {
+      std::memcpy(dst, src, n);
+      return;
+    }
+    std::lock_guard<std::mutex> one_job(job_m_);
+    uint64_t my_gen;
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      dst_ = static_cast<uint8_t *>(dst);
+      src_ = static_cast<const uint8_t *>(src);
+      n_ = n;
+      const size_t parts = workers_.size() + 1;
+      piece_ = ((n + parts - 1) / parts + 4095) & ~(size_t)4095;
+      npieces_ = (n + piece_ - 1) / piece_;
+      remaining_ = npieces_;
+      next_.store(0);
+      my_gen = ++gen_;
+    }
+    cv_.notify_all();
+    work(my_gen);
+    std::unique_lock<std::mutex> lk(m_);
+    done_cv_.wait(lk, [&] { return remaining_ == 0; });
+  }
+  size_t threads() const { return workers_.size() + 1; }
+
+ private:
+  CopyPool() {
+    const char *env = std::getenv("PP_HOST_COPY_THREADS");
+    unsigned hw = std::thread::hardware_concurrency();
+    // 3/4 of the host threads, at most 12 (scripts/host_stage_sweep.py)
+    long want = env ? std::strtol(env, nullptr, 10) : (long)std::min(12u, std::max(1u, hw * 3 / 4));
+    for (long i = 1; i < want; ++i) workers_.emplace_back([this] { loop(); });
+    for (auto &t : workers_) t.detach();
+  }
+  void work(uint64_t gen) {
+    for (;;) {
+      size_t i;
+      uint8_t *d;
+      const uint8_t *s;
+      size_t len;
+      {
+        std::lock_guard<std::mutex> lk(m_);
+        if (gen != gen_) return;
+        i = next_.fetch_add(1);
+        if (i >= npieces_) return;
+        const size_t off = i * piece_;
+        d = dst_ + off;
+        s = src_ + off;
+        len = std::min(piece_, n_ - off);
+      }
+      std::memcpy(d, s, len);
+      std::lock_guard<std::mutex> lk(m_);
+      if (--remaining_ == 0) done_cv_.notify_all();
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      uint64_t g;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        g = seen = gen_;
+      }
+      work(g);
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_, job_m_;
+  std::condition_variable cv_, done_cv_;
+  uint8_t *dst_ = nullptr;
+  const uint8_t *src_ = nullptr;
+  size_t n_ = 0, piece_ = 0, npieces_ = 0, remaining_ = 0;
+  std::atomic<size_t> next_{0};
+  uint64_t gen_ = 0;
+};
 
 struct HostCtx {
   int dev = -1;
   cudaStream_t copy = nullptr, count = nullptr;
   void *buf[kNbuf] = {};
+  void *pinned[kNbuf] = {};  // staging for pageable sources (allocated on first use)
   cudaEvent_t copied[kNbuf] = {}, freed[kNbuf] = {};
   unsigned long long *dcnt = nullptr;
   unsigned long long *hcnt = nullptr;  // pinned
@@ -233,9 +329,10 @@ struct HostCtx {
     cudaSetDevice(dev);
     for (int i = 0; i < kNbuf; ++i) {
       if (buf[i]) cudaFree(buf[i]);
+      if (pinned[i]) cudaFreeHost(pinned[i]);
       if (copied[i]) cudaEventDestroy(copied[i]);
       if (freed[i]) cudaEventDestroy(freed[i]);
-      buf[i] = nullptr;
+      buf[i] = pinned[i] = nullptr;
       copied[i] = freed[i] = nullptr;
     }
     if (dcnt) cudaFree(dcnt);
@@ -264,8 +361,23 @@ struct HostCtx {
     if ((e = cudaMallocHost(&hcnt, 64 * sizeof(unsigned long long)))) return e;
     return cudaSuccess;
   }
+  cudaError_t ensure_pinned() {
+    cudaError_t e;
+    for (int i = 0; i < kNbuf; ++i)
+      if (!pinned[i] && (e = cudaMallocHost(&pinned[i], kChunk))) return e;
+    return cudaSuccess;
+  }
 };
 thread_local HostCtx g_host;
+
+bool host_is_pinned(const void *p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
 }  // namespace
 
 int pp_count_host(const void *host_data, size_t nbytes, int width,
@@ -285,15 +397,34 @@ int pp_count_host(const void *host_data, size_t nbytes, int width,
   cudaError_t e = g_host.ensure(dev);
   if (e != cudaSuccess) return cuda_fail(e, "pp_count_host setup");
   HostCtx &h = g_host;
+  // below ~32 MiB the driver's own pageable staging is as fast
+  const bool staged = !host_is_pinned(host_data) && nbytes >= (32u << 20);
+  // staged chunks are smaller so the pool copy of chunk i+1 overlaps the DMA
+  // of chunk i even for inputs of a few chunks
+  static const size_t stage_chunk = [] {
+    const char *env = std::getenv("PP_HOST_STAGE_CHUNK");
+    size_t c = env ? (size_t)std::strtoull(env, nullptr, 10) : (size_t)(8u << 20);
+    c &= ~(size_t)63;
+    return (c < (1u << 20) || c > kChunk) ? (size_t)(8u << 20) : c;
+  }();
+  const size_t chunk = staged ? stage_chunk : kChunk;
+  if (staged && (e = h.ensure_pinned())) return cuda_fail(e, "pp_count_host staging");
   if ((e = cudaMemsetAsync(h.dcnt, 0, 64 * sizeof(unsigned long long), h.count)))
     return cuda_fail(e, "cudaMemsetAsync");
   const uint8_t *src = static_cast<const uint8_t *>(host_data);
   size_t off = 0;
   for (size_t i = 0; off < nbytes; ++i) {
     const int b = (int)(i % kNbuf);
-    const size_t len = (nbytes - off) < kChunk ? (nbytes - off) : kChunk;
+    const size_t len = (nbytes - off) < chunk ? (nbytes - off) : chunk;
+    const void *from = src + off;
+    if (staged) {
+      // pinned[b] is free once the H2D copy of chunk i - NBUF has completed
+      if ((e = cudaEventSynchronize(h.copied[b]))) return cuda_fail(e, "staging wait");
+      CopyPool::get().copy(h.pinned[b], src + off, len);
+      from = h.pinned[b];
+    }
     if ((e = cudaStreamWaitEvent(h.copy, h.freed[b], 0))) return cuda_fail(e, "wait freed");
-    if ((e = cudaMemcpyAsync(h.buf[b], src + off, len, cudaMemcpyHostToDevice, h.copy)))
+    if ((e = cudaMemcpyAsync(h.buf[b], from, len, cudaMemcpyHostToDevice, h.copy)))
       return cuda_fail(e, "cudaMemcpyAsync H2D");
     if ((e = cudaEventRecord(h.copied[b], h.copy))) return cuda_fail(e, "record copied");
     if ((e = cudaStreamWaitEvent(h.count, h.copied[b], 0))) return cuda_fail(e, "wait copied");
