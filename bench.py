@@ -271,7 +271,10 @@ def main_gpu(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # under torchrun (even with one rank) the NCCL path runs: every step ends
+    # with the allreduce of the counters; plain `python bench.py` is N=1 local
+    use_dist = "LOCAL_RANK" in os.environ or world > 1
+    if use_dist:
         dist.init_process_group("nccl", device_id=dev)
     lib = _lib.load()
     st = torch.cuda.current_stream(dev)
@@ -298,8 +301,19 @@ def main_gpu(args):
     view_ptr = buf.data_ptr() + offset
     torch.cuda.synchronize()
 
-    counters = torch.zeros(64, dtype=torch.int64, device=dev)
-    glob = torch.zeros(64, dtype=torch.int64, device=dev)
+    # counters2[p] accumulates the steps of parity p.  Exchange pipeline: the
+    # side stream snapshots counters2[i % 2] after step i's count and
+    # allreduces the snapshot while the main stream counts step i+1 into the
+    # other accumulator; the main stream only ever carries count kernels (plus
+    # waits), and the timed region waits for every exchange (drain()).
+    counters2 = torch.zeros((2, 64), dtype=torch.int64, device=dev)
+    counters = counters2[0]
+    globs = [torch.zeros(64, dtype=torch.int64, device=dev) for _ in range(2)]
+    count_ev = [torch.cuda.Event() for _ in range(2)]
+    snap_ev = [torch.cuda.Event() for _ in range(2)]
+    red_ev = [torch.cuda.Event() for _ in range(2)]
+    side = torch.cuda.Stream(dev) if use_dist else None
+    nstep = [0]
     seg_out = None
     if cfg == "c4seg":
         seg = 4096
@@ -307,19 +321,34 @@ def main_gpu(args):
         seg_out = torch.zeros((nseg, w), dtype=torch.int64, device=dev)
 
     def step():
+        b = nstep[0] % 2
         if seg_out is not None:
             _lib.check(lib.pp_count_fixed(view_ptr, 4096, nbytes // 4096, w, seg_out.data_ptr(),
                                           _lib.PP_SEG_OVERWRITE, sp))
         else:
-            _lib.check(lib.pp_count(view_ptr, nbytes, w, counters.data_ptr(), sp))
-        if world > 1:
-            glob.copy_(counters)
-            dist.all_reduce(glob)
+            if use_dist:
+                st.wait_event(snap_ev[b])  # step i-2's snapshot of counters2[b] is taken
+            _lib.check(lib.pp_count(view_ptr, nbytes, w, counters2[b].data_ptr(), sp))
+        if use_dist:
+            count_ev[b].record(st)
+            side.wait_event(count_ev[b])
+            with torch.cuda.stream(side):
+                side.wait_event(red_ev[b])  # globs[b] free again
+                globs[b].copy_(counters2[b])
+                snap_ev[b].record(side)
+                dist.all_reduce(globs[b])
+                red_ev[b].record(side)
+        nstep[0] += 1
+
+    def drain():
+        if use_dist:  # the last exchanges complete inside the timed region
+            st.wait_event(red_ev[0])
+            st.wait_event(red_ev[1])
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
 
@@ -330,32 +359,34 @@ def main_gpu(args):
         e0.record(st)
         for _ in range(args.steps):
             step()
+        drain()
         e1.record(st)
         torch.cuda.synchronize()
         clk.mark(False)
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     t_ms = e0.elapsed_time(e1)
-    if world == 1:
+    if not use_dist:
         # each step is exactly one launch of the dominant kernel
         k_ms = t_ms / args.steps
     else:
         # kernel alone (no allreduce between launches), same stream, same clocks
         k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         k0.record(st)
+        scratch = torch.zeros(64, dtype=torch.int64, device=dev)
         for _ in range(args.steps):
-            _lib.check(lib.pp_count(view_ptr, nbytes, w, counters.data_ptr(), sp))
+            _lib.check(lib.pp_count(view_ptr, nbytes, w, scratch.data_ptr(), sp))
         k1.record(st)
         torch.cuda.synchronize()
         k_ms = k0.elapsed_time(k1) / args.steps
-    if world > 1:
+    if use_dist:
         tt = torch.tensor([t_ms, k_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms, k_ms = tt.tolist()
     per_step_bytes = nbytes  # this rank's bytes per step
     job_bytes = per_step_bytes
-    if world > 1:
+    if use_dist:
         jb = torch.tensor([per_step_bytes], dtype=torch.int64, device=dev)
         dist.all_reduce(jb)
         job_bytes = int(jb.item())
@@ -366,7 +397,7 @@ def main_gpu(args):
     exact = None
     if args.check and cfg == "c5" and rank == 0:
         want = golden_total("c5_w16_64gib_total")
-        src = glob if world > 1 else counters
+        src = (globs[0] + globs[1]) if use_dist else counters2.sum(0)
         got = src.cpu().numpy().view(np.uint64)[:w]
         total = args.warmup + args.steps
         exact = None if want is None else bool(
@@ -375,8 +406,8 @@ def main_gpu(args):
         from oracle import oracle as O
         host = buf.cpu().numpy()
         want = O.hs512(host, offset, nbytes, w, threads=host_threads())
-        got = counters.cpu().numpy().view(np.uint64)[:w]
-        total = args.warmup + args.steps + (args.steps if world > 1 else 0)
+        got = counters2.sum(0).cpu().numpy().view(np.uint64)[:w]
+        total = args.warmup + args.steps
         exact = bool(all(int(g) == total * x for g, x in zip(got, want)))
         del host
 
@@ -418,13 +449,13 @@ def main_gpu(args):
         nst = max(2, min(args.steps, 5))
         for _ in range(1):
             pp.pospopcnt(pinned, w)
-        if world > 1:
+        if use_dist:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(nst):
             res = pp.pospopcnt(pinned, w)  # H2D inside, D2H of the w counters
         t_e2e = time.perf_counter() - t0
-        if world > 1:
+        if use_dist:
             tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t_e2e = tt.item()
@@ -474,7 +505,7 @@ def main_gpu(args):
             "exact": exact,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
     return 0
 
