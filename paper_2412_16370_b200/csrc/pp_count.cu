@@ -35,6 +35,9 @@ constexpr int kLdgChunkVecs = kLdgThreads * 8;
 constexpr unsigned long long kLdgChunkBytes = kLdgChunkVecs * 16ull;
 
 constexpr int kSegThreads = 256;
+#ifndef PP_SEG_SMEM_COUNTS
+#define PP_SEG_SMEM_COUNTS true
+#endif
 #ifndef PP_SEG_MIN_BLOCKS
 #define PP_SEG_MIN_BLOCKS 3  // <= 85 registers: 24 warps/SM of loads in flight
 #endif
@@ -248,9 +251,9 @@ __device__ __forceinline__ bool seg_partial(const SegGeom &g, unsigned long long
 // (frame bits G*f + r and 32 + G*f + r), rotated by rot = 8*(p0 mod 8) and
 // folded mod w exactly like flush_fw (accumulate.py:115-130).  All G lanes of
 // the group call this together (they share s).
-template <int G>
+template <int G, bool SM>
 __device__ __forceinline__ void write_row(const SegArgs &a, unsigned long long s,
-                                          uintptr_t p0, const GroupCounter<G> &c,
+                                          uintptr_t p0, const GroupCounter<G, SM> &c,
                                           uint32_t lane) {
   constexpr int S = 32 / G;
   const int w = a.width;
@@ -263,8 +266,8 @@ __device__ __forceinline__ void write_row(const SegArgs &a, unsigned long long s
     for (int f = 0; f < S; ++f) {
       const int pe = G * f + r;
       unsigned long long *de = row + ((pe - rot) & 63), *dd = row + ((pe + 32 - rot) & 63);
-      *de = ow ? c.ce[f] : *de + c.ce[f];
-      *dd = ow ? c.co[f] : *dd + c.co[f];
+      *de = ow ? c.e(f) : *de + c.e(f);
+      *dd = ow ? c.o(f) : *dd + c.o(f);
     }
   } else if (G <= w) {
     // lane r's positions G*f + r fall in w/G classes mod w; class of f is f % nc
@@ -275,7 +278,7 @@ __device__ __forceinline__ void write_row(const SegArgs &a, unsigned long long s
         unsigned long long tot = 0ull;
 #pragma unroll
         for (int f = cc; f < S; ++f)
-          if (f % nc == cc) tot += c.ce[f] + c.co[f];
+          if (f % nc == cc) tot += c.e(f) + c.o(f);
         unsigned long long *d = row + ((G * cc + r - rot) & (w - 1));
         *d = ow ? tot : *d + tot;
       }
@@ -285,7 +288,7 @@ __device__ __forceinline__ void write_row(const SegArgs &a, unsigned long long s
     // the group share a class.
     unsigned long long tot = 0ull;
 #pragma unroll
-    for (int f = 0; f < S; ++f) tot += c.ce[f] + c.co[f];
+    for (int f = 0; f < S; ++f) tot += c.e(f) + c.o(f);
     const unsigned gmask =
         (G == 32) ? FULL : (((1u << G) - 1u) << (lane & ~(uint32_t)(G - 1)));
     for (int m = w; m < G; m <<= 1) tot += __shfl_xor_sync(gmask, tot, m);
@@ -305,6 +308,7 @@ template <int G>
 __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
     pp_seg_kernel(SegArgs a) {
   constexpr int S = 32 / G;
+  __shared__ unsigned long long slots[(kSegThreads / 32) * 2 * S * 32];
   const uint32_t lane = threadIdx.x & 31, r = lane % G, sl = lane / G;
   const unsigned long long gw = (blockIdx.x * (unsigned long long)kSegThreads + threadIdx.x) >> 5;
   const unsigned long long nw = (gridDim.x * (unsigned long long)kSegThreads) >> 5;
@@ -312,8 +316,8 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
   for (unsigned long long first = gw * S; first < a.nseg; first += nw * S) {
     const unsigned long long s = first + sl;
     const SegGeom g = seg_geom(a, s);
-    GroupCounter<G> c;
-    c.init();
+    GroupCounter<G, PP_SEG_SMEM_COUNTS> c;
+    c.init(slots + (threadIdx.x >> 5) * (2 * S * 32) + lane);
     // full (aligned, in-range) vectors are [kf0, kf1)
     const unsigned long long kf0 = g.hp ? 1 : 0;
     const unsigned long long kf1 = (g.tp && g.nvv) ? g.nvv - 1 : g.nvv;
@@ -346,7 +350,7 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
       c.eat8(v, t);
     }
     c.finish(t);
-    if (s < a.nseg) write_row<G>(a, s, g.p0, c, lane);
+    if (s < a.nseg) write_row(a, s, g.p0, c, lane);
   }
 }
 

@@ -228,20 +228,37 @@ __device__ __forceinline__ uint32_t gtranspose(uint32_t x, const TC &t) {
   return x;
 }
 
-template <int G>
+// SMEM = true keeps the 2S exact u64 counts of each lane in shared memory
+// (slot i of lane l at sc[i*32 + l], conflict-free): they are touched only
+// when planes are flushed, and dropping them from registers lets 32 warps
+// per SM stay resident (more loads in flight).
+template <int G, bool SMEM = false>
 struct GroupCounter {
   static_assert(G == 8 || G == 16 || G == 32, "lanes per segment");
   static constexpr int S = 32 / G;  // positions per lane per tree
   Planes l1e, l1o, l2e, l2o;
   uint32_t l2n;
   // lane r of a segment's group: frame bits G*f + r (e) and 32 + G*f + r (o)
-  unsigned long long ce[S], co[S];
+  unsigned long long ce[SMEM ? 1 : S], co[SMEM ? 1 : S];
+  unsigned long long *sc;  // SMEM: this lane's slot 0 (stride 32)
 
-  __device__ __forceinline__ void init() {
+  __device__ __forceinline__ void init(unsigned long long *slots = nullptr) {
     l1e = l1o = l2e = l2o = Planes{0u, 0u, 0u, 0u};
     l2n = 0;
+    sc = slots;
 #pragma unroll
-    for (int f = 0; f < S; ++f) ce[f] = co[f] = 0ull;
+    for (int f = 0; f < S; ++f) {
+      if (SMEM) {
+        sc[f * 32] = 0ull;
+        sc[(S + f) * 32] = 0ull;
+      } else {
+        ce[f] = co[f] = 0ull;
+      }
+    }
+  }
+  __device__ __forceinline__ unsigned long long e(int f) const { return SMEM ? sc[f * 32] : ce[f]; }
+  __device__ __forceinline__ unsigned long long o(int f) const {
+    return SMEM ? sc[(S + f) * 32] : co[f];
   }
 
   static __device__ __forceinline__ uint32_t field_popc(uint32_t x, int f) {
@@ -270,8 +287,13 @@ struct GroupCounter {
     }
 #pragma unroll
     for (int f = 0; f < S; ++f) {
-      ce[f] += (unsigned long long)se[f] << shift;
-      co[f] += (unsigned long long)so[f] << shift;
+      if (SMEM) {
+        sc[f * 32] += (unsigned long long)se[f] << shift;
+        sc[(S + f) * 32] += (unsigned long long)so[f] << shift;
+      } else {
+        ce[f] += (unsigned long long)se[f] << shift;
+        co[f] += (unsigned long long)so[f] << shift;
+      }
     }
   }
 
