@@ -109,17 +109,38 @@ def test_reference_package_drives_b200_kernel_object():
     ref = importlib.util.module_from_spec(spec)
     sys.modules["pospopcnt_ref_t"] = ref
     old = sys.dont_write_bytecode
-    sys.dont_write_bytecode = True
+    sys.dont_write_bytecode = True  # never write into the reference tree
     try:
         spec.loader.exec_module(ref)
+        _drive_reference(ref)
     finally:
         sys.dont_write_bytecode = old
+
+
+def _drive_reference(ref):
     k = kernels.B200Kernel()
     with pytest.raises(ref.InputLengthError):
         ref.pospopcnt(b"\x00" * 7, 64, kernel=k)
     if not k.available():
         with pytest.raises(ref.KernelUnavailableError):
             ref.pospopcnt(b"\x01\x80", 16, kernel=k)
+    # register into the reference's own registry
+    from paper_2412_16370_b200.ref_plugin import register
+    reg_k = register(ref)
+    assert register(ref) is reg_k  # idempotent
+    assert ref.get_kernel("b200") is reg_k
+    names = [d.name for d, _ in ref.list_kernels()]
+    assert names[0] == "portable" and "b200" in names  # reference contract kept
+    assert ref.select_kernel().name != "b200"  # default dispatch unchanged
+    from importlib import import_module
+    ref_bench = import_module("pospopcnt_ref_t.bench")
+    if reg_k.available():
+        assert callable(ref_bench._resolve_runner("b200"))
+    else:
+        with pytest.raises(ref.KernelUnavailableError):
+            ref_bench._resolve_runner("b200")
+        with pytest.raises(ref.KernelUnavailableError):
+            ref.select_kernel("b200")
 
 
 def test_registry_contract(monkeypatch):
