@@ -411,6 +411,25 @@ def main_gpu(args):
         exact = bool(all(int(g) == total * x for g, x in zip(got, want)))
         del host
 
+    # the metric is per word width: the same resident bytes at every other w
+    # (one launch per step, CUDA events around the steps, this rank's GB/s)
+    per_width = None
+    if seg_out is None and cfg == "c2":
+        per_width = {}
+        scratch_w = torch.zeros(64, dtype=torch.int64, device=dev)
+        for ww in (8, 16, 32, 64):
+            if nbytes % (ww // 8):
+                continue
+            for _ in range(2):
+                _lib.check(lib.pp_count(view_ptr, nbytes, ww, scratch_w.data_ptr(), sp))
+            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            q0.record(st)
+            for _ in range(args.steps):
+                _lib.check(lib.pp_count(view_ptr, nbytes, ww, scratch_w.data_ptr(), sp))
+            q1.record(st)
+            torch.cuda.synchronize()
+            per_width[str(ww)] = round(nbytes * args.steps / (q0.elapsed_time(q1) / 1e3) / 1e9, 1)
+
     # the paper's read-only "roofline" kernel over the same bytes
     sink = torch.zeros(1, dtype=torch.int64, device=dev)
     for _ in range(max(3, args.warmup)):
@@ -503,6 +522,7 @@ def main_gpu(args):
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
             "exact": exact,
+            "per_width_gbs": per_width,
         }
         print(json.dumps(line), flush=True)
     if use_dist:
