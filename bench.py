@@ -47,6 +47,8 @@ CONFIGS = {
     "c3": ("onehot32", 32, 4 * GIB, "w=32 one-hot, 4 GiB, bounded Zipf(1.1) over 32 bits"),
     "c4": ("bernoulli", 64, 64 * MIB, "w=64, 64 MiB at byte offset 3, Bernoulli(0.01)"),
     "c4seg": ("bernoulli", 64, GIB, "w=64, 262,144 segments x 4 KiB, Bernoulli(0.01)"),
+    "c3cat": ("codes8", 32, GIB, "w=32 GROUP BY COUNT: 2^30 u8 category codes with C3's Zipf "
+                                  "draws, fused one-hot producer (pp_count_categories)"),
     "c5": ("blocks", 16, 64 * GIB, "w=16, 64 GiB array sharded over the GPUs (8 GiB per GPU "
                                    "at N=8), Bernoulli(p) with p ~ U[0,1] per 1 MiB block"),
 }
@@ -284,7 +286,9 @@ def main_gpu(args):
     kind, w, nbytes, desc = CONFIGS[cfg]
     if args.width and cfg in ("c2",):
         w = args.width
-    seed = {"c1": 0xC1, "c2": 0xC2, "c3": 0xC3, "c4": 0xC4, "c4seg": 0xC4 + 1, "c5": 0xC5}[cfg]
+    seed = {"c1": 0xC1, "c2": 0xC2, "c3": 0xC3, "c4": 0xC4, "c4seg": 0xC4 + 1, "c5": 0xC5,
+            "c3cat": 0xC3}[cfg]
+    categorical = cfg == "c3cat"
     offset = 3 if cfg == "c4" else 0
     word_unit = 4 if kind == "onehot32" else 8
     strong = cfg in STRONG
@@ -328,7 +332,11 @@ def main_gpu(args):
         else:
             if use_dist:
                 st.wait_event(snap_ev[b])  # step i-2's snapshot of counters2[b] is taken
-            _lib.check(lib.pp_count(view_ptr, nbytes, w, counters2[b].data_ptr(), sp))
+            if categorical:  # one u8 code per byte
+                _lib.check(lib.pp_count_categories(view_ptr, nbytes, 1, w,
+                                                   counters2[b].data_ptr(), sp))
+            else:
+                _lib.check(lib.pp_count(view_ptr, nbytes, w, counters2[b].data_ptr(), sp))
         if use_dist:
             count_ev[b].record(st)
             side.wait_event(count_ev[b])
@@ -402,6 +410,13 @@ def main_gpu(args):
         total = args.warmup + args.steps
         exact = None if want is None else bool(
             all(int(g) == total * x for g, x in zip(got, want)))
+    elif args.check and categorical and rank == 0 and not use_dist:
+        # same draws as C3's one-hot words: the reference's own C3 counters
+        with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
+            want = {c["name"]: c for c in json.load(f)["cases"]}["c3_w32_onehot_4gib"]["numba"]
+        got = counters2.sum(0).cpu().numpy().view(np.uint64)[:w]
+        total = args.warmup + args.steps
+        exact = bool(all(int(g) == total * x for g, x in zip(got, want)))
     elif args.check and cfg in ("c1", "c2", "c3", "c4") and rank == 0:
         from oracle import oracle as O
         host = buf.cpu().numpy()
@@ -445,7 +460,8 @@ def main_gpu(args):
 
     peak, peak_src = load_peaks()
     achieved = per_step_bytes / (k_ms / 1e3) / 1e9
-    kernel_key = "pp_seg_kernel" if seg_out is not None else "pp_tma_kernel<true>"
+    kernel_key = ("pp_seg_kernel" if seg_out is not None else
+                  "pp_cat_kernel<1>" if categorical else "pp_tma_kernel<true>")
     traffic, traffic_ratio = load_traffic(kernel_key, per_step_bytes)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -466,13 +482,14 @@ def main_gpu(args):
         pinned.copy_(buf[offset:offset + nbytes])
         torch.cuda.synchronize()
         nst = max(2, min(args.steps, 5))
+        api = pp.pospopcnt_categories if categorical else pp.pospopcnt
         for _ in range(1):
-            pp.pospopcnt(pinned, w)
+            api(pinned, w)
         if use_dist:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(nst):
-            res = pp.pospopcnt(pinned, w)  # H2D inside, D2H of the w counters
+            res = api(pinned, w)  # H2D inside, D2H of the w counters
         t_e2e = time.perf_counter() - t0
         if use_dist:
             tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
@@ -486,7 +503,7 @@ def main_gpu(args):
         del pinned, res
 
     cpu = None
-    if args.cpu_baseline and world == 1 and rank == 0 and seg_out is None:
+    if args.cpu_baseline and world == 1 and rank == 0 and seg_out is None and not categorical:
         sample = min(nbytes, 256 * MIB)
         host = buf[offset:offset + sample].cpu().numpy()
         gbs, threads, _, k, t = time_cpu_port(host, w, args.cpu_min_time)

@@ -119,6 +119,19 @@ PP_API int pp_count_frame(const void *data, size_t nbytes, unsigned long long *f
                           void *stream);
 
 /*
+ * pp_count_categories — fused one-hot producer + count (
+ * the paper's GROUP BY COUNT use case):
+ *   counters[j] += #{i < ncodes : codes[i] == j},  j < width
+ * i.e. exactly pospopcnt(one_hot_width(codes), width) without materialising
+ * the one-hot words (codes >= width have no bit in a width-bit word).
+ * codes: DEVICE array of ncodes unsigned integers of code_bytes (1, 2, 4),
+ * aligned to code_bytes.  Replaces Kernel.run over one-hot words
+ * (kernels.py:242-270) for categorical inputs.
+ */
+PP_API int pp_count_categories(const void *codes, size_t ncodes, int code_bytes, int width,
+                               unsigned long long *counters, void *stream);
+
+/*
  * pp_readonly_sum — the paper's "roofline" dummy kernel:
  * streams nbytes through exactly the load path of pp_count and XORs them into
  * *sink (DEVICE, 1 uint64).  Measurement only.
@@ -141,6 +154,9 @@ PP_API int pp_gen_bernoulli(void *dst, size_t nbytes, uint64_t seed, uint64_t wo
 PP_API int pp_gen_blocks(void *dst, size_t nbytes, uint64_t seed, uint64_t word_offset,
                   uint64_t block_bytes, void *stream);
 /* one-hot u32 words: bit = #{k < 31 : thresholds[k] <= u}, u uniform u32 */
+/* u8 codes with the same draws: code i = bit position of one-hot word i    */
+PP_API int pp_gen_codes8(void *dst, size_t n, uint64_t seed, uint64_t offset,
+                         const uint32_t *thresholds31, void *stream);
 PP_API int pp_gen_onehot32(void *dst, size_t nbytes, uint64_t seed, uint64_t word_offset,
                     const uint32_t *thresholds31, void *stream);
 

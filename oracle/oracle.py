@@ -60,6 +60,8 @@ def lib():
         L.oracle_gen_bernoulli.argtypes = [u8p, sz, u64, u64, ctypes.c_uint32]
         L.oracle_gen_blocks.argtypes = [u8p, sz, u64, u64, u64]
         L.oracle_gen_onehot32.argtypes = [u8p, sz, u64, u64, u8p]
+        L.oracle_gen_codes8.argtypes = [u8p, sz, u64, u64, u8p]
+        L.oracle_gen_codes8.restype = None
         L.oracle_block_q.argtypes = [u64, u64]
         L.oracle_block_q.restype = ctypes.c_uint32
         for f in (L.oracle_gen_uniform, L.oracle_gen_bernoulli, L.oracle_gen_blocks,
@@ -199,6 +201,20 @@ def gen_onehot32(nbytes, seed, thr=None, word_offset=0):
     out = np.empty(nbytes // 4, dtype=np.uint32)
     lib().oracle_gen_onehot32(out.ctypes.data, out.size, seed, word_offset, thr.ctypes.data)
     return out.view(np.uint8)
+
+
+def gen_codes8(n, seed, thr=None, word_offset=0):
+    thr = zipf_thresholds() if thr is None else np.ascontiguousarray(thr, dtype=np.uint32)
+    out = np.empty(n, dtype=np.uint8)
+    lib().oracle_gen_codes8(out.ctypes.data, out.size, seed, word_offset, thr.ctypes.data)
+    return out
+
+
+def categories(codes, w):
+    """GROUP BY COUNT oracle: #{i : codes[i] == j} for j < w (== pospopcnt of one-hot words)."""
+    c = np.asarray(codes).astype(np.int64).ravel()
+    c = c[(c >= 0) & (c < w)]
+    return [int(x) for x in np.bincount(c, minlength=w)[:w]]
 
 
 def onehot_expected(nwords, seed, thr=None, word_offset=0):

@@ -408,6 +408,16 @@ void oracle_gen_onehot32(uint32_t *dst, size_t nwords, uint64_t seed, uint64_t o
   }
 }
 
+void oracle_gen_codes8(uint8_t *dst, size_t n, uint64_t seed, uint64_t off,
+                       const uint32_t *thr31) {
+  for (size_t i = 0; i < n; ++i) {
+    const uint32_t u = (uint32_t)(mix64(seed + (off + i + 1ull) * GOLDEN) >> 32);
+    uint32_t cat = 0;
+    for (int k = 0; k < 31; ++k) cat += thr31[k] <= u;
+    dst[i] = (uint8_t)cat;
+  }
+}
+
 /* per-block q values of oracle_gen_blocks (for closed-form expectations) */
 uint32_t oracle_block_q(uint64_t seed, uint64_t b) {
   return (uint32_t)(mix64((seed ^ BLOCK_SALT) + (b + 1ull) * GOLDEN) % 65537ull);

@@ -31,6 +31,7 @@ SIGNATURES = {
     "pp_count": (_int, [_vp, _sz, _int, _vp, _vp]),
     "pp_count_host": (_int, [_vp, _sz, _int, _vp]),
     "pp_count_frame": (_int, [_vp, _sz, _vp, _vp]),
+    "pp_count_categories": (_int, [_vp, _sz, _int, _int, _vp, _vp]),
     "pp_count_segmented": (_int, [_vp, _vp, _sz, _int, _vp, _int, _vp]),
     "pp_count_fixed": (_int, [_vp, _sz, _sz, _int, _vp, _int, _vp]),
     "pp_readonly_sum": (_int, [_vp, _sz, _vp, _vp]),
@@ -38,6 +39,7 @@ SIGNATURES = {
     "pp_gen_bernoulli": (_int, [_vp, _sz, _u64, _u64, _u32, _vp]),
     "pp_gen_blocks": (_int, [_vp, _sz, _u64, _u64, _u64, _vp]),
     "pp_gen_onehot32": (_int, [_vp, _sz, _u64, _u64, _vp, _vp]),
+    "pp_gen_codes8": (_int, [_vp, _sz, _u64, _u64, _vp, _vp]),
 }
 
 _lock = threading.Lock()

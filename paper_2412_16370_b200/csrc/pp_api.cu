@@ -142,6 +142,46 @@ int pp_count_frame(const void *data, size_t nbytes, unsigned long long *frame64,
   return count_device(data, nbytes, 64, frame64, static_cast<cudaStream_t>(stream), di, true);
 }
 
+int pp_count_categories(const void *codes, size_t ncodes, int code_bytes, int width,
+                        unsigned long long *counters, void *stream) {
+  if (!width_ok(width)) return fail(PP_EWIDTH, "word width must be one of (8, 16, 32, 64), got %d", width);
+  if (code_bytes != 1 && code_bytes != 2 && code_bytes != 4)
+    return fail(PP_EARG, "code_bytes must be 1, 2 or 4, got %d", code_bytes);
+  int rc;
+  if ((rc = check_device_ptr(counters, "counters"))) return rc;
+  if (ncodes == 0) return PP_OK;
+  if ((rc = check_device_ptr(codes, "codes"))) return rc;
+  if ((uintptr_t)codes % (uintptr_t)code_bytes)
+    return fail(PP_EARG, "codes must be %d-byte aligned", code_bytes);
+  pp::DevInfo di;
+  if ((rc = current_devinfo(&di))) return rc;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaError_t e;
+  // u8 codes at w <= 32: one-hot expansion on the TMA pipeline; w = 64 and
+  // wider codes: shared-memory histogram columns (scripts/cat_ab.py)
+  const char *force = std::getenv("PP_CAT_PATH");
+  const bool onehot = force ? std::strcmp(force, "onehot") == 0 : width <= 32;
+  if (code_bytes == 1 && onehot) {
+    // u8 codes: expand to packed one-hot words in registers and run the
+    // carry-save counter on the TMA pipeline (frame position = code mod w)
+    pp::CountArgs a{};
+    pp::split_range(static_cast<const uint8_t *>(codes), ncodes, pp::codes8_chunk_bytes(), &a);
+    a.counters = counters;
+    a.width = width;
+    a.rot = 0;
+    e = pp::launch_count_codes8(a, di, static_cast<cudaStream_t>(stream));
+  } else {
+    // 2- / 4-byte codes (and the A/B alternative for u8): per-thread shared
+    // memory histogram columns
+    e = pp::launch_categories(static_cast<const uint8_t *>(codes),
+                              (unsigned long long)ncodes * code_bytes, code_bytes, width,
+                              counters, di, dev, static_cast<cudaStream_t>(stream));
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "pp_count_categories launch");
+  return PP_OK;
+}
+
 // Lanes per segment: explicit hint in flags bits 8-15, else from the
 // (average) segment size: one warp per segment from 16 KiB up, 8 lanes
 // (4 segments per warp, 4x fewer transposes per segment) below 8 KiB.
@@ -474,6 +514,17 @@ int pp_gen_blocks(void *dst, size_t nbytes, uint64_t seed, uint64_t word_offset,
   cudaError_t e = pp::launch_gen_blocks(static_cast<uint64_t *>(dst), nbytes / 8, seed,
                                         word_offset, block_bytes, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? PP_OK : cuda_fail(e, "pp_gen_blocks");
+}
+
+int pp_gen_codes8(void *dst, size_t n, uint64_t seed, uint64_t offset,
+                  const uint32_t *thresholds31, void *stream) {
+  int rc;
+  if (!thresholds31) return fail(PP_EARG, "thresholds31 is NULL");
+  if (n == 0) return PP_OK;
+  if ((rc = check_device_ptr(dst, "dst"))) return rc;
+  cudaError_t e = pp::launch_gen_codes8(static_cast<uint8_t *>(dst), n, seed, offset,
+                                        thresholds31, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? PP_OK : cuda_fail(e, "pp_gen_codes8");
 }
 
 int pp_gen_onehot32(void *dst, size_t nbytes, uint64_t seed, uint64_t word_offset,

@@ -29,6 +29,21 @@ constexpr int kTmaStageVecs = kTmaConsumerWarps * 32 * 8;  // 2048 x 16 B = 32 K
 constexpr unsigned long long kTmaStageBytes = kTmaStageVecs * 16ull;
 constexpr size_t kTmaSmemBytes = kTmaStages * kTmaStageBytes + 2 * kTmaStages * 8;
 
+// Shape of the TMA pipeline for NCW consumer warps (8 vectors per thread per
+// stage).  The counting kernel uses 8 warps; the fused one-hot producer does
+// ~4x more ALU work per byte and uses more consumer warps.
+template <int NCW>
+struct TmaShape {
+  static constexpr int kThreads = (NCW + 1) * 32;
+  static constexpr int kStageVecs = NCW * 32 * 8;
+  static constexpr unsigned long long kStageBytes = kStageVecs * 16ull;
+  static constexpr size_t kSmem = kTmaStages * kStageBytes + 2 * kTmaStages * 8;
+};
+#ifndef PP_CAT_NCW
+#define PP_CAT_NCW 16
+#endif
+using CatShape = TmaShape<PP_CAT_NCW>;
+
 constexpr int kLdgWarps = 8;
 constexpr int kLdgThreads = kLdgWarps * 32;
 constexpr int kLdgChunkVecs = kLdgThreads * 8;
@@ -71,12 +86,140 @@ __device__ __forceinline__ void fold_frame_to_counters(const unsigned long long 
   }
 }
 
-template <bool kCount>
-__global__ void __launch_bounds__(kTmaThreads, 1)
+// ---- fused one-hot producer (pp_count_categories on u8 codes) -------------
+// A code c < W becomes bit c of a one-hot word; words are packed so that the
+// frame position of that bit is = c (mod W) and the epilogue is the plain
+// fold with rot = 0:  W=8: four codes per word (byte k holds 1 << code_k),
+// W=16: two codes per word (half k), W=32: one code per word, W=64: one code
+// per (x|z = bits 0-31, y|w = bits 32-63) pair.  Codes >= W give no bit.
+
+// 4 u8 codes -> 4 one-hot bytes.  PRMT against the table {1,2,4,...,128}
+// turns nibble-packed codes into one-hot bytes in one instruction; bytes
+// whose code is >= 8 are cleared only when such a byte is present.
+__device__ __forceinline__ uint32_t onehot8x4(uint32_t x, bool any_big) {
+  const uint32_t xl = x & 0x07070707u;
+  const uint32_t tt = xl | (xl >> 4);
+  const uint32_t sel = (tt & 0xFFu) | ((tt >> 8) & 0xFF00u);
+  uint32_t oh = __byte_perm(0x08040201u, 0x80402010u, sel);
+  if (any_big) {
+    const uint32_t hi = x & 0xF8F8F8F8u;
+    const uint32_t nz = (((hi & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | hi) & 0x80808080u;
+    oh &= ~((nz >> 7) * 0xFFu);
+  }
+  return oh;
+}
+// 2 u8 codes (bytes k, k+1 of x) -> one word with 16-bit one-hot halves
+__device__ __forceinline__ uint32_t onehot16x2(uint32_t x, int k) {
+  const uint32_t a = (x >> (8 * k)) & 0xFFu, b = (x >> (8 * k + 8)) & 0xFFu;
+  uint32_t lo, hi;
+  asm("shl.b32 %0, 1, %1;" : "=r"(lo) : "r"(a));        // >= 32 -> 0 (clamped)
+  asm("shl.b32 %0, 65536, %1;" : "=r"(hi) : "r"(b));    // >= 16 -> 0
+  return (lo & 0xFFFFu) | hi;
+}
+__device__ __forceinline__ uint32_t onehot32(uint32_t c) {
+  uint32_t r;
+  asm("shl.b32 %0, 1, %1;" : "=r"(r) : "r"(c));  // c >= 32 -> 0
+  return r;
+}
+
+// Expand and count 8 vectors (128 u8 codes) of one thread; vectors with
+// valid bit i clear are absent (partial last chunk) and contribute nothing.
+template <int W>
+__device__ __forceinline__ void eat_codes(Counter &c, const uint4 (&v)[8], uint32_t valid,
+                                          const TC &t) {
+  if (W == 8) {
+    uint4 u[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const bool big = ((v[i].x | v[i].y | v[i].z | v[i].w) & 0xF8F8F8F8u) != 0;
+      u[i] = make_uint4(onehot8x4(v[i].x, big), onehot8x4(v[i].y, big),
+                        onehot8x4(v[i].z, big), onehot8x4(v[i].w, big));
+      if (!((valid >> i) & 1u)) u[i] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    c.eat8(u, t);
+  } else if (W == 16) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint4 u[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint4 x = v[4 * h + i];
+        const bool ok = (valid >> (4 * h + i)) & 1u;
+        u[2 * i] = ok ? make_uint4(onehot16x2(x.x, 0), onehot16x2(x.x, 2), onehot16x2(x.y, 0),
+                                   onehot16x2(x.y, 2))
+                      : make_uint4(0u, 0u, 0u, 0u);
+        u[2 * i + 1] = ok ? make_uint4(onehot16x2(x.z, 0), onehot16x2(x.z, 2),
+                                       onehot16x2(x.w, 0), onehot16x2(x.w, 2))
+                          : make_uint4(0u, 0u, 0u, 0u);
+      }
+      c.eat8(u, t);
+    }
+  } else if (W == 32) {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      uint4 u[8];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const uint4 x = v[2 * h + i];
+        const bool ok = (valid >> (2 * h + i)) & 1u;
+        const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t wd = w4[q];
+          u[4 * i + q] = ok ? make_uint4(onehot32(wd & 0xFFu), onehot32((wd >> 8) & 0xFFu),
+                                         onehot32((wd >> 16) & 0xFFu), onehot32(wd >> 24))
+                            : make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
+      c.eat8(u, t);
+    }
+  } else {  // W == 64: code c -> (x|z, y|w) = (1 << c, 1 << (c - 32))
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const uint4 x = v[h];
+      const bool ok = (valid >> h) & 1u;
+      const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+      uint4 u[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const uint32_t c0 = (w4[q] >> (16 * k)) & 0xFFu, c1 = (w4[q] >> (16 * k + 8)) & 0xFFu;
+          u[2 * q + k] = ok ? make_uint4(onehot32(c0), onehot32(c0 - 32u), onehot32(c1),
+                                         onehot32(c1 - 32u))
+                            : make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
+      c.eat8(u, t);
+    }
+  }
+}
+
+// Head/tail codes (< 16 each) of the fused producer: frame position = code.
+__device__ __forceinline__ void count_code_edges(Counter &c, const uint8_t *head, uint32_t hb,
+                                                 const uint8_t *tail, uint32_t tb, uint32_t lane,
+                                                 int width, const TC &t) {
+  uint32_t code = 0xFFu;
+  if (lane < 16) {
+    if (lane < hb) code = __ldg(head + lane);
+  } else if (lane - 16 < tb) {
+    code = __ldg(tail + (lane - 16));
+  }
+  const bool ok = code < (uint32_t)width;
+  c.ce += wcount(ok ? onehot32(code) : 0u, t);
+  c.co += wcount(ok ? onehot32(code - 32u) : 0u, t);
+}
+
+// MODE 0: read-only roofline (XOR of every word), MODE 1: positional count,
+// MODE 8/16/32/64: fused one-hot producer over u8 codes at that width.
+template <int MODE, int NCW = kTmaConsumerWarps>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1)
     pp_tma_kernel(CountArgs a, unsigned long long *sink) {
+  constexpr bool kCount = MODE != 0;
+  using Sh = TmaShape<NCW>;
   extern __shared__ __align__(128) uint8_t smem[];
   uint4 *stages = reinterpret_cast<uint4 *>(smem);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kTmaStages * kTmaStageBytes);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kTmaStages * Sh::kStageBytes);
   uint64_t *empty = full + kTmaStages;
   __shared__ unsigned long long frame[64];
 
@@ -84,7 +227,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTmaStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kTmaConsumerWarps);
+      mbar_init(&empty[s], NCW);
     }
     fence_mbar_init();
   }
@@ -92,18 +235,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   __syncthreads();
 
   const unsigned long long nchunks = a.nchunks;
-  if (warp == kTmaConsumerWarps) {
+  if (warp == NCW) {
     // ---------------- producer: one elected thread issues bulk copies
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       uint32_t stage = 0, phase = 0;
       for (unsigned long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
         mbar_wait(&empty[stage], phase ^ 1);
-        const unsigned long long off = ch * kTmaStageBytes;
+        const unsigned long long off = ch * Sh::kStageBytes;
         const unsigned long long rem = a.body_bytes - off;
-        const uint32_t bytes = (uint32_t)(rem < kTmaStageBytes ? rem : kTmaStageBytes);
+        const uint32_t bytes = (uint32_t)(rem < Sh::kStageBytes ? rem : Sh::kStageBytes);
         mbar_arrive_expect_tx(&full[stage], bytes);
-        bulk_g2s(stages + stage * kTmaStageVecs, a.body + off, bytes, &full[stage], pol);
+        bulk_g2s(stages + stage * Sh::kStageVecs, a.body + off, bytes, &full[stage], pol);
         if (++stage == kTmaStages) {
           stage = 0;
           phase ^= 1;
@@ -120,25 +263,30 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     const uint32_t tid = threadIdx.x;
     for (unsigned long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
       mbar_wait(&full[stage], phase);
-      const uint4 *sv = stages + stage * kTmaStageVecs;
+      const uint4 *sv = stages + stage * Sh::kStageVecs;
       uint4 v[8];
-      const unsigned long long off = ch * kTmaStageBytes;
+      uint32_t valid = 0xFFu;  // vectors present in this (possibly partial) chunk
+      const unsigned long long off = ch * Sh::kStageBytes;
       const unsigned long long rem = a.body_bytes - off;
-      if (rem >= kTmaStageBytes) {
+      if (rem >= Sh::kStageBytes) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = sv[tid + i * (kTmaConsumerWarps * 32)];
+        for (int i = 0; i < 8; ++i) v[i] = sv[tid + i * (NCW * 32)];
       } else {
         const uint32_t nv = (uint32_t)(rem >> 4);
+        valid = 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const uint32_t idx = tid + i * (kTmaConsumerWarps * 32);
+          const uint32_t idx = tid + i * (NCW * 32);
           v[i] = idx < nv ? sv[idx] : make_uint4(0u, 0u, 0u, 0u);
+          valid |= (idx < nv ? 1u : 0u) << i;
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
-      if (kCount) {
+      if (MODE == 1) {
         c.eat8(v, t);
+      } else if (MODE >= 8) {
+        eat_codes<(MODE >= 8 ? MODE : 8)>(c, v, valid, t);
       } else {
 #pragma unroll
         for (int i = 0; i < 8; ++i) xs ^= v[i].x ^ v[i].y ^ v[i].z ^ v[i].w;
@@ -150,8 +298,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     }
     if (kCount) {
       c.finish(t);
-      if (blockIdx.x == 0 && warp == 0)
-        count_edges(c, a.head, a.head_bytes, a.tail, a.tail_bytes, lane, t);
+      if (blockIdx.x == 0 && warp == 0) {
+        if (MODE == 1)
+          count_edges(c, a.head, a.head_bytes, a.tail, a.tail_bytes, lane, t);
+        else
+          count_code_edges(c, a.head, a.head_bytes, a.tail, a.tail_bytes, lane, a.width, t);
+      }
       atomicAdd(&frame[lane], c.ce);
       atomicAdd(&frame[32 + lane], c.co);
     } else {
@@ -370,6 +522,8 @@ void split_range(const uint8_t *data, unsigned long long nbytes,
   a->rot = (int)(8u * ((uintptr_t)data & 7u));
 }
 
+unsigned long long codes8_chunk_bytes() { return CatShape::kStageBytes; }
+
 unsigned long long count_chunk_bytes(LoadPath path) {
   return path == LoadPath::kTma ? kTmaStageBytes : kLdgChunkBytes;
 }
@@ -383,12 +537,17 @@ cudaError_t device_info(int dev, DevInfo *out) {
     if ((e = cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev))) return e;
     if ((e = cudaDeviceGetAttribute(&d.cc_major, cudaDevAttrComputeCapabilityMajor, dev))) return e;
     if ((e = cudaDeviceGetAttribute(&d.cc_minor, cudaDevAttrComputeCapabilityMinor, dev))) return e;
-    if ((e = cudaFuncSetAttribute(pp_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((e = cudaFuncSetAttribute(pp_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kTmaSmemBytes)))
       return e;
-    if ((e = cudaFuncSetAttribute(pp_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((e = cudaFuncSetAttribute(pp_tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kTmaSmemBytes)))
       return e;
+    for (auto k : {pp_tma_kernel<8, PP_CAT_NCW>, pp_tma_kernel<16, PP_CAT_NCW>,
+                   pp_tma_kernel<32, PP_CAT_NCW>, pp_tma_kernel<64, PP_CAT_NCW>})
+      if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)CatShape::kSmem)))
+        return e;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.seg_blocks_per_sm,
                                                            pp_seg_kernel<8>, kSegThreads, 0)))
       return e;
@@ -413,7 +572,7 @@ cudaError_t launch_count(const CountArgs &a, LoadPath path, const DevInfo &di,
                          cudaStream_t st) {
   if (path == LoadPath::kTma) {
     const unsigned g = grid_for(a.nchunks, (unsigned long long)di.num_sms);
-    pp_tma_kernel<true><<<g, kTmaThreads, kTmaSmemBytes, st>>>(a, nullptr);
+    pp_tma_kernel<1><<<g, kTmaThreads, kTmaSmemBytes, st>>>(a, nullptr);
   } else {
     const unsigned g =
         grid_for(a.nchunks, (unsigned long long)di.num_sms * di.ldg_blocks_per_sm);
@@ -422,10 +581,29 @@ cudaError_t launch_count(const CountArgs &a, LoadPath path, const DevInfo &di,
   return cudaGetLastError();
 }
 
+cudaError_t launch_count_codes8(const CountArgs &a, const DevInfo &di, cudaStream_t st) {
+  const unsigned g = grid_for(a.nchunks, (unsigned long long)di.num_sms);
+  switch (a.width) {
+    case 8:
+      pp_tma_kernel<8, PP_CAT_NCW><<<g, CatShape::kThreads, CatShape::kSmem, st>>>(a, nullptr);
+      break;
+    case 16:
+      pp_tma_kernel<16, PP_CAT_NCW><<<g, CatShape::kThreads, CatShape::kSmem, st>>>(a, nullptr);
+      break;
+    case 32:
+      pp_tma_kernel<32, PP_CAT_NCW><<<g, CatShape::kThreads, CatShape::kSmem, st>>>(a, nullptr);
+      break;
+    default:
+      pp_tma_kernel<64, PP_CAT_NCW><<<g, CatShape::kThreads, CatShape::kSmem, st>>>(a, nullptr);
+      break;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_readonly(const CountArgs &a, unsigned long long *sink, const DevInfo &di,
                             cudaStream_t st) {
   const unsigned g = grid_for(a.nchunks, (unsigned long long)di.num_sms);
-  pp_tma_kernel<false><<<g, kTmaThreads, kTmaSmemBytes, st>>>(a, sink);
+  pp_tma_kernel<0><<<g, kTmaThreads, kTmaSmemBytes, st>>>(a, sink);
   return cudaGetLastError();
 }
 

@@ -11,6 +11,7 @@
 //   blocks         bernoulli with q_b = mix64((seed ^ SALT) + (b+1) GOLDEN) mod 65537
 //                  for block b = (8 g) / block_bytes
 //   onehot32       u32 word g = 1 << #{k < 31 : thr[k] <= hi32(mix64(seed + (g+1) GOLDEN))}
+//   codes8         u8 code g = that same bit position (one_hot(codes8) == onehot32)
 #include "pp_internal.h"
 
 namespace pp {
@@ -77,6 +78,20 @@ __global__ void gen_onehot32_kernel(uint32_t *dst, unsigned long long n, uint64_
   }
 }
 
+// u8 category codes with the C3 distribution: code i = the bit position of
+// onehot32 word i (same draws), so one_hot(codes8[i]) == onehot32[i].
+__global__ void gen_codes8_kernel(uint8_t *dst, unsigned long long n, uint64_t seed,
+                                  uint64_t off, Thr31 thr) {
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint32_t u = (uint32_t)(mix64(seed + (off + i + 1ull) * GOLDEN) >> 32);
+    uint32_t cat = 0;
+#pragma unroll
+    for (int k = 0; k < 31; ++k) cat += (thr.t[k] <= u) ? 1u : 0u;
+    dst[i] = (uint8_t)cat;
+  }
+}
+
 static unsigned gen_grid(unsigned long long n) {
   unsigned long long g = (n + 255) / 256;
   const unsigned long long cap = 148ull * 16;
@@ -108,6 +123,15 @@ cudaError_t launch_gen_onehot32(uint32_t *dst, unsigned long long n, uint64_t se
   Thr31 t;
   for (int k = 0; k < 31; ++k) t.t[k] = thr31[k];
   gen_onehot32_kernel<<<gen_grid(n), 256, 0, st>>>(dst, n, seed, off, t);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gen_codes8(uint8_t *dst, unsigned long long n, uint64_t seed, uint64_t off,
+                              const uint32_t *thr31, cudaStream_t st) {
+  if (!n) return cudaSuccess;
+  Thr31 t;
+  for (int k = 0; k < 31; ++k) t.t[k] = thr31[k];
+  gen_codes8_kernel<<<gen_grid(n), 256, 0, st>>>(dst, n, seed, off, t);
   return cudaGetLastError();
 }
 

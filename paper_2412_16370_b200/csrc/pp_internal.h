@@ -50,12 +50,21 @@ void split_range(const uint8_t *data, unsigned long long nbytes,
                  unsigned long long chunk_bytes, CountArgs *a);
 
 unsigned long long count_chunk_bytes(LoadPath path);
+unsigned long long codes8_chunk_bytes();
 cudaError_t launch_count(const CountArgs &a, LoadPath path, const DevInfo &di,
                          cudaStream_t st);
 cudaError_t launch_segmented(const SegArgs &a, const DevInfo &di, cudaStream_t st);
+// fused one-hot producer over u8 codes (a.width = W, a.rot ignored)
+cudaError_t launch_count_codes8(const CountArgs &a, const DevInfo &di, cudaStream_t st);
 cudaError_t launch_readonly(const CountArgs &a, unsigned long long *sink,
                             const DevInfo &di, cudaStream_t st);
 
+cudaError_t launch_categories(const uint8_t *codes, unsigned long long nbytes, int code_bytes,
+                              int ncat, unsigned long long *counters, const DevInfo &di,
+                              int dev, cudaStream_t st);
+
+cudaError_t launch_gen_codes8(uint8_t *dst, unsigned long long n, uint64_t seed,
+                              uint64_t offset, const uint32_t *thr31, cudaStream_t st);
 cudaError_t launch_gen_uniform(uint64_t *dst, unsigned long long nwords, uint64_t seed,
                                uint64_t word_offset, cudaStream_t st);
 cudaError_t launch_gen_bernoulli(uint64_t *dst, unsigned long long nwords, uint64_t seed,

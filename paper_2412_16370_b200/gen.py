@@ -8,6 +8,7 @@ stand in for the configs' distributions:
   bernoulli   C4: i.i.d. Bernoulli(q/65536) bits (q=655 -> p=0.009995)
   blocks      C5: Bernoulli(q_b/65536) with q_b uniform on [0, 65536] per block
   onehot32    C3: u32 words with one set bit, bounded Zipf(1.1) over 32 positions
+  codes8      C3 as u8 category codes (code i = bit position of onehot32 word i)
 """
 
 import numpy as np
@@ -46,6 +47,9 @@ def generate(kind, nbytes, seed, device="cuda", word_offset=0, q=655,
         elif kind == "onehot32":
             thr = zipf_thresholds()
             rc = lib.pp_gen_onehot32(ptr, nbytes, seed, word_offset, thr.ctypes.data, st)
+        elif kind == "codes8":  # one u8 code per byte; one_hot(code i) == onehot32 word i
+            thr = zipf_thresholds()
+            rc = lib.pp_gen_codes8(ptr, nbytes, seed, word_offset, thr.ctypes.data, st)
         else:
             raise ValueError(f"unknown generator {kind!r}")
     _lib.check(rc)

@@ -1,0 +1,78 @@
+"""GPU parity of the fused one-hot producer (pospopcnt_categories).
+
+Contract: pospopcnt_categories(codes, w) == pospopcnt(one_hot_w(codes), w)
+== bincount of the codes below w.  Pinned to the reference through config
+C3: the u8 codes generated with C3's draws must reproduce the reference's own
+counters of the 4 GiB one-hot array (tests/golden/golden.json).
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden.json")
+
+
+def test_c3_codes_equal_reference_onehot_counts(cuda):
+    torch, pp = cuda
+    from paper_2412_16370_b200 import gen
+    with open(GOLDEN) as f:
+        case = {c["name"]: c for c in json.load(f)["cases"]}["c3_w32_onehot_4gib"]
+    codes = gen.generate("codes8", 1 << 30, 0xC3)  # 2^30 codes, one per byte
+    assert pp.pospopcnt_categories(codes, 32) == case["numba"]
+    onehot = gen.generate("onehot32", 4 << 30, 0xC3)
+    assert pp.pospopcnt(onehot, 32) == case["numba"]
+    del codes, onehot
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("dtype", ("uint8", "int16", "int32"))
+def test_random_codes_vs_oracle_and_materialised_onehot(cuda, oracle, dtype):
+    torch, pp = cuda
+    rng = np.random.default_rng(7)
+    tdt = {"uint8": torch.uint8, "int16": torch.int16, "int32": torch.int32}[dtype]
+    for n in (0, 1, 15, 16, 17, 1000, 65536 + 7, 3_000_001):
+        hi = 80 if dtype == "uint8" else 200  # some codes >= w: not counted
+        host = rng.integers(0, hi, n).astype(dtype)
+        full = torch.from_numpy(np.concatenate([np.zeros(3, dtype), host])).cuda()
+        codes = full[3:]  # start 3 codes into the allocation (unaligned to 16 B)
+        for w in (8, 16, 32, 64):
+            want = oracle.categories(host, w)
+            assert pp.pospopcnt_categories(codes, w) == want, (dtype, n, w)
+            if n and n <= 65536 + 7 and w in (16, 64):
+                oh = np.where(host.astype(np.int64) < w,
+                              np.left_shift(np.uint64(1), np.minimum(host, w - 1).astype(np.uint64)),
+                              np.uint64(0))
+                words = oh.astype({16: np.uint16, 64: np.uint64}[w])
+                assert pp.pospopcnt(torch.from_numpy(words.view(np.uint8)).cuda(), w) == want
+    c = torch.ones(32, dtype=torch.int64, device="cuda")
+    codes = torch.from_numpy(rng.integers(0, 32, 10_000).astype(np.uint8)).cuda()
+    pp.pospopcnt_categories(codes, 32, counters=c)
+    want = oracle.categories(codes.cpu().numpy(), 32)
+    assert [int(x) for x in c.cpu()] == [v + 1 for v in want]
+
+
+def test_u16_column_split_across_launches(cuda):
+    """Every code in one bin: each thread's u16 column sits at its 65535 limit
+    and the launch is split; the total must still be exact."""
+    torch, pp = cuda
+    n = (10 << 30) + 5
+    codes = torch.full((n,), 7, dtype=torch.uint8, device="cuda")
+    got = pp.pospopcnt_categories(codes, 8)
+    assert got == [0] * 7 + [n]
+    del codes
+    torch.cuda.empty_cache()
+
+
+def test_errors(cuda):
+    torch, pp = cuda
+    with pytest.raises(ValueError):
+        pp.pospopcnt_categories(torch.zeros(4, dtype=torch.float32, device="cuda"), 8)
+    with pytest.raises(ValueError):
+        pp.pospopcnt_categories(torch.zeros(4, dtype=torch.uint8, device="cuda"), 12)
+    with pytest.raises(ValueError):
+        pp.pospopcnt_categories(torch.zeros(4, dtype=torch.uint8, device="cuda"), 16,
+                                counters=[0] * 8)
