@@ -3,25 +3,30 @@
 
 Default (N=1): BASELINE.json configs[1] = C2, w=8 over a 1 GiB array of
 Bernoulli(0.5) bits generated in place in HBM.  One step = one pass of the
-hot path (pp_count, one launch of the sm_100a kernel) over the whole array;
-under torchrun (N>1) each rank counts its own 1 GiB shard of an N GiB array
-(weak scaling) and each step ends with the NCCL allreduce of the counters.
+hot path (pp_count, one launch of the sm_100a kernel) over the whole array.
+Under torchrun (any N, NCCL) each rank counts its own 1 GiB shard of an
+N GiB array (weak scaling) and each step's counters are allreduced,
+pipelined on a side stream; ``--config c5`` is the fixed 64 GiB array split
+over the N ranks (strong scaling).
 
 Printed JSON keys beyond the base contract:
-  roofline      dominant kernel: algorithmic bytes per launch (n input bytes,
-                SURVEY.md 8d) / mean launch time vs MEASURED_PEAKS.hbm_gbs
-  cpu_baseline  the reference's fastest CPU path (C restatement of
-                NumbaKernel.run, oracle/) on the host's cores, bounded sample
-  e2e           the same metric through the public API pospopcnt() on a
-                pinned HOST buffer: H2D copies + D2H of the counters inside
-                the timed region
-  exact         counters after all steps == steps x CPU oracle (C2 only)
+  roofline       dominant kernel: algorithmic bytes per launch (n input bytes,
+                 SURVEY.md 8d) / mean launch time vs MEASURED_PEAKS.hbm_gbs,
+                 plus the in-run read-only roofline kernel and ncu traffic
+  cpu_baseline   the reference's fastest CPU path (C restatement of
+                 NumbaKernel.run, oracle/) on the host's cores, bounded sample
+  e2e            the same metric through the public API pospopcnt() on a
+                 pinned HOST buffer: H2D copies + D2H of the counters inside
+                 the timed region
+  exact          counters after all steps == steps x expected (CPU oracle, or
+                 the reference's own golden totals for C3 codes / C5)
+  per_width_gbs  C2 bytes counted at every word width (the metric is per w)
+  clocks         NVML SM clock / throttle reasons sampled inside the region
 
 ``--impl reference`` times the reference's CPU implementation (the oracle
 port; the reference itself is Python and is not on the GPU box) on the same
-config with all host threads.  ``--config`` selects another BASELINE config
-(c1, c3, c4, c4seg, c5) for an extra line; ``--sweep`` prints one line per
-word width.
+config with all host threads.  ``--config`` selects another config (c1, c3,
+c3cat, c4, c4seg, c5) for an extra line.
 """
 
 import argparse
@@ -98,7 +103,8 @@ class ClockSampler:
         0x4: "sw_power_cap",
     }
 
-    def __init__(self, index, period=0.001):
+    def __init__(self, index, period=None):
+        period = float(os.environ.get("PP_BENCH_CLOCK_PERIOD", "0.001")) if period is None else period
         self.index, self.period = index, period
         self.samples = []  # (t, sm_mhz, reasons_mask)
         self.t0 = self.t1 = None
@@ -177,6 +183,14 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
                 "samples": len(inside), "window": window,
                 "source": "nvml" if self.nvml is not None else "nvidia-smi"}
+
+
+def gpu_busy(ms=1.0):
+    """Queue a ~ms spin kernel on the current stream before a start event, so
+    the timed launches are already queued when the event fires (the timed
+    region then measures device throughput, not host launch latency)."""
+    import torch
+    torch.cuda._sleep(int(ms * 2.0e6))  # ~2e6 cycles per ms at ~2 GHz
 
 
 def host_threads():
@@ -364,6 +378,7 @@ def main_gpu(args):
     with ClockSampler(local) as clk:
         time.sleep(0.05)  # let the sampler start before the timed region
         clk.mark(True)
+        gpu_busy()  # launches queue behind a spin, not an idle GPU
         e0.record(st)
         for _ in range(args.steps):
             step()
@@ -381,6 +396,7 @@ def main_gpu(args):
     else:
         # kernel alone (no allreduce between launches), same stream, same clocks
         k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        gpu_busy()  # launches queue behind a spin, not an idle GPU
         k0.record(st)
         scratch = torch.zeros(64, dtype=torch.int64, device=dev)
         for _ in range(args.steps):
@@ -438,6 +454,7 @@ def main_gpu(args):
             for _ in range(2):
                 _lib.check(lib.pp_count(view_ptr, nbytes, ww, scratch_w.data_ptr(), sp))
             q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            gpu_busy()  # launches queue behind a spin, not an idle GPU
             q0.record(st)
             for _ in range(args.steps):
                 _lib.check(lib.pp_count(view_ptr, nbytes, ww, scratch_w.data_ptr(), sp))
@@ -451,6 +468,7 @@ def main_gpu(args):
         _lib.check(lib.pp_readonly_sum(view_ptr, nbytes, sink.data_ptr(), sp))
     r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     nro = max(5, args.steps)
+    gpu_busy()  # launches queue behind a spin, not an idle GPU
     r0.record(st)
     for _ in range(nro):
         _lib.check(lib.pp_readonly_sum(view_ptr, nbytes, sink.data_ptr(), sp))
