@@ -479,7 +479,7 @@ def main_gpu(args):
     peak, peak_src = load_peaks()
     achieved = per_step_bytes / (k_ms / 1e3) / 1e9
     kernel_key = ("pp_seg_kernel" if seg_out is not None else
-                  "pp_cat_kernel<1>" if categorical else "pp_tma_kernel<true>")
+                  "pp_cat_kernel<1>" if categorical else "pp_tma_kernel<1>")
     traffic, traffic_ratio = load_traffic(kernel_key, per_step_bytes)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,

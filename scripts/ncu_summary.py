@@ -38,8 +38,8 @@ def short(name):
     for k in ("pp_tma_kernel<1>", "pp_tma_kernel<0>", "pp_tma_kernel<true>", "pp_tma_kernel<false>",
               "pp_seg_kernel", "pp_count_ldg_kernel", "gen_"):
         if k in name:
-            return {"pp_tma_kernel<1>": "pp_tma_kernel<true>",
-                    "pp_tma_kernel<0>": "pp_tma_kernel<false>"}.get(k, k)
+            return {"pp_tma_kernel<true>": "pp_tma_kernel<1>",
+                    "pp_tma_kernel<false>": "pp_tma_kernel<0>"}.get(k, k)
     return name[:40]
 
 
