@@ -16,7 +16,7 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=3)
-    ap.add_argument("--which", default="count,readonly,seg")
+    ap.add_argument("--which", default="count,readonly,seg,cat")
     ap.add_argument("--width", type=int, default=8)
     args = ap.parse_args()
     import torch
@@ -33,6 +33,7 @@ def main():
     sink = torch.zeros(1, dtype=torch.int64, device=dev)
     out = torch.zeros((n // 4096, 64), dtype=torch.int64, device=dev)
     which = args.which.split(",")
+    codes = gen.generate("codes8", n, 0xC3, device=dev) if "cat" in which else None
     for _ in range(args.reps):
         if "count" in which:
             _lib.check(lib.pp_count(buf.data_ptr(), n, args.width, cnt.data_ptr(), sp))
@@ -41,6 +42,9 @@ def main():
         if "seg" in which:
             _lib.check(lib.pp_count_fixed(seg_buf.data_ptr(), 4096, n // 4096, 64,
                                           out.data_ptr(), _lib.PP_SEG_OVERWRITE, sp))
+        if "cat" in which:  # one-hot path (w=32) and histogram path (w=64)
+            for w in (32, 64):
+                _lib.check(lib.pp_count_categories(codes.data_ptr(), n, 1, w, cnt.data_ptr(), sp))
     torch.cuda.synchronize()
     print("ok", [int(x) for x in cnt[:args.width].cpu()][:4])
 
