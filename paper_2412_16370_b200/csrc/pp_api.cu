@@ -158,10 +158,11 @@ int pp_count_categories(const void *codes, size_t ncodes, int code_bytes, int wi
   int dev = 0;
   cudaGetDevice(&dev);
   cudaError_t e;
-  // u8 codes at w <= 32: one-hot expansion on the TMA pipeline; w = 64 and
-  // wider codes: shared-memory histogram columns (scripts/cat_ab.py)
+  // u8 codes: one-hot expansion on the TMA pipeline (faster at every width,
+  // profiles/r1_categories_ablation.md); 2- / 4-byte codes: shared-memory
+  // histogram columns.  PP_CAT_PATH=smem|onehot forces a path (A/B runs).
   const char *force = std::getenv("PP_CAT_PATH");
-  const bool onehot = force ? std::strcmp(force, "onehot") == 0 : width <= 32;
+  const bool onehot = force ? std::strcmp(force, "onehot") == 0 : true;
   if (code_bytes == 1 && onehot) {
     // u8 codes: expand to packed one-hot words in registers and run the
     // carry-save counter on the TMA pipeline (frame position = code mod w)

@@ -108,9 +108,13 @@ __device__ __forceinline__ uint32_t onehot8x4(uint32_t x, bool any_big) {
   }
   return oh;
 }
+// byte k of x, zero-extended: one PRMT
+__device__ __forceinline__ uint32_t byte_of(uint32_t x, int k) {
+  return __byte_perm(x, 0u, 0x4440u | (uint32_t)k);
+}
 // 2 u8 codes (bytes k, k+1 of x) -> one word with 16-bit one-hot halves
 __device__ __forceinline__ uint32_t onehot16x2(uint32_t x, int k) {
-  const uint32_t a = (x >> (8 * k)) & 0xFFu, b = (x >> (8 * k + 8)) & 0xFFu;
+  const uint32_t a = byte_of(x, k), b = byte_of(x, k + 1);
   uint32_t lo, hi;
   asm("shl.b32 %0, 1, %1;" : "=r"(lo) : "r"(a));        // >= 32 -> 0 (clamped)
   asm("shl.b32 %0, 65536, %1;" : "=r"(hi) : "r"(b));    // >= 16 -> 0
@@ -124,9 +128,11 @@ __device__ __forceinline__ uint32_t onehot32(uint32_t c) {
 
 // Expand and count 8 vectors (128 u8 codes) of one thread; vectors with
 // valid bit i clear are absent (partial last chunk) and contribute nothing.
-template <int W>
+// FULL: every vector present (all but the last chunk) -- no per-word selects.
+template <int W, bool FULL>
 __device__ __forceinline__ void eat_codes(Counter &c, const uint4 (&v)[8], uint32_t valid,
                                           const TC &t) {
+  const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
   if (W == 8) {
     uint4 u[8];
 #pragma unroll
@@ -134,7 +140,7 @@ __device__ __forceinline__ void eat_codes(Counter &c, const uint4 (&v)[8], uint3
       const bool big = ((v[i].x | v[i].y | v[i].z | v[i].w) & 0xF8F8F8F8u) != 0;
       u[i] = make_uint4(onehot8x4(v[i].x, big), onehot8x4(v[i].y, big),
                         onehot8x4(v[i].z, big), onehot8x4(v[i].w, big));
-      if (!((valid >> i) & 1u)) u[i] = make_uint4(0u, 0u, 0u, 0u);
+      if (!FULL && !((valid >> i) & 1u)) u[i] = z4;
     }
     c.eat8(u, t);
   } else if (W == 16) {
@@ -144,13 +150,13 @@ __device__ __forceinline__ void eat_codes(Counter &c, const uint4 (&v)[8], uint3
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const uint4 x = v[4 * h + i];
-        const bool ok = (valid >> (4 * h + i)) & 1u;
+        const bool ok = FULL || ((valid >> (4 * h + i)) & 1u);
         u[2 * i] = ok ? make_uint4(onehot16x2(x.x, 0), onehot16x2(x.x, 2), onehot16x2(x.y, 0),
                                    onehot16x2(x.y, 2))
-                      : make_uint4(0u, 0u, 0u, 0u);
+                      : z4;
         u[2 * i + 1] = ok ? make_uint4(onehot16x2(x.z, 0), onehot16x2(x.z, 2),
                                        onehot16x2(x.w, 0), onehot16x2(x.w, 2))
-                          : make_uint4(0u, 0u, 0u, 0u);
+                          : z4;
       }
       c.eat8(u, t);
     }
@@ -161,14 +167,14 @@ __device__ __forceinline__ void eat_codes(Counter &c, const uint4 (&v)[8], uint3
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const uint4 x = v[2 * h + i];
-        const bool ok = (valid >> (2 * h + i)) & 1u;
+        const bool ok = FULL || ((valid >> (2 * h + i)) & 1u);
         const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const uint32_t wd = w4[q];
-          u[4 * i + q] = ok ? make_uint4(onehot32(wd & 0xFFu), onehot32((wd >> 8) & 0xFFu),
-                                         onehot32((wd >> 16) & 0xFFu), onehot32(wd >> 24))
-                            : make_uint4(0u, 0u, 0u, 0u);
+          u[4 * i + q] = ok ? make_uint4(onehot32(wd & 0xFFu), onehot32(byte_of(wd, 1)),
+                                         onehot32(byte_of(wd, 2)), onehot32(wd >> 24))
+                            : z4;
         }
       }
       c.eat8(u, t);
@@ -177,17 +183,17 @@ __device__ __forceinline__ void eat_codes(Counter &c, const uint4 (&v)[8], uint3
 #pragma unroll
     for (int h = 0; h < 8; ++h) {
       const uint4 x = v[h];
-      const bool ok = (valid >> h) & 1u;
+      const bool ok = FULL || ((valid >> h) & 1u);
       const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
       uint4 u[8];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-          const uint32_t c0 = (w4[q] >> (16 * k)) & 0xFFu, c1 = (w4[q] >> (16 * k + 8)) & 0xFFu;
+          const uint32_t c0 = byte_of(w4[q], 2 * k), c1 = byte_of(w4[q], 2 * k + 1);
           u[2 * q + k] = ok ? make_uint4(onehot32(c0), onehot32(c0 - 32u), onehot32(c1),
                                          onehot32(c1 - 32u))
-                            : make_uint4(0u, 0u, 0u, 0u);
+                            : z4;
         }
       }
       c.eat8(u, t);
@@ -286,7 +292,10 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       if (MODE == 1) {
         c.eat8(v, t);
       } else if (MODE >= 8) {
-        eat_codes<(MODE >= 8 ? MODE : 8)>(c, v, valid, t);
+        if (valid == 0xFFu)
+          eat_codes<(MODE >= 8 ? MODE : 8), true>(c, v, valid, t);
+        else
+          eat_codes<(MODE >= 8 ? MODE : 8), false>(c, v, valid, t);
       } else {
 #pragma unroll
         for (int i = 0; i < 8; ++i) xs ^= v[i].x ^ v[i].y ^ v[i].z ^ v[i].w;
