@@ -299,7 +299,6 @@ class CopyPool {
     std::unique_lock<std::mutex> lk(m_);
     done_cv_.wait(lk, [&] { return remaining_ == 0; });
   }
-  size_t threads() const { return workers_.size() + 1; }
 
  private:
   CopyPool() {
