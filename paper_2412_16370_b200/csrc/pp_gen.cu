@@ -25,6 +25,15 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+// Every generator lets a programmatic dependent launch start immediately
+// (PDL trigger at entry), before a single output byte is written.  The
+// counting kernels launched behind it must therefore honour the PDL
+// contract -- griddepcontrol.wait before their first read -- and the
+// generate-then-count tests check exactly that.
+__device__ __forceinline__ void pdl_trigger_now() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ uint64_t ladder(uint64_t seed, uint64_t g, uint32_t q) {
   if (q >= 65536u) return ~0ull;
   uint64_t x = 0;
@@ -39,6 +48,7 @@ __device__ __forceinline__ uint64_t ladder(uint64_t seed, uint64_t g, uint32_t q
 
 __global__ void gen_uniform_kernel(uint64_t *dst, unsigned long long n, uint64_t seed,
                                    uint64_t off) {
+  pdl_trigger_now();
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x)
     dst[i] = mix64(seed + (off + i + 1ull) * GOLDEN);
@@ -46,6 +56,7 @@ __global__ void gen_uniform_kernel(uint64_t *dst, unsigned long long n, uint64_t
 
 __global__ void gen_bernoulli_kernel(uint64_t *dst, unsigned long long n, uint64_t seed,
                                      uint64_t off, uint32_t q) {
+  pdl_trigger_now();
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x)
     dst[i] = ladder(seed, off + i, q);
@@ -53,6 +64,7 @@ __global__ void gen_bernoulli_kernel(uint64_t *dst, unsigned long long n, uint64
 
 __global__ void gen_blocks_kernel(uint64_t *dst, unsigned long long n, uint64_t seed,
                                   uint64_t off, uint64_t block_bytes) {
+  pdl_trigger_now();
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const uint64_t g = off + i;
@@ -68,6 +80,7 @@ struct Thr31 {
 
 __global__ void gen_onehot32_kernel(uint32_t *dst, unsigned long long n, uint64_t seed,
                                     uint64_t off, Thr31 thr) {
+  pdl_trigger_now();
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const uint32_t u = (uint32_t)(mix64(seed + (off + i + 1ull) * GOLDEN) >> 32);
@@ -82,6 +95,7 @@ __global__ void gen_onehot32_kernel(uint32_t *dst, unsigned long long n, uint64_
 // onehot32 word i (same draws), so one_hot(codes8[i]) == onehot32[i].
 __global__ void gen_codes8_kernel(uint8_t *dst, unsigned long long n, uint64_t seed,
                                   uint64_t off, Thr31 thr) {
+  pdl_trigger_now();
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const uint32_t u = (uint32_t)(mix64(seed + (off + i + 1ull) * GOLDEN) >> 32);
@@ -92,9 +106,25 @@ __global__ void gen_codes8_kernel(uint8_t *dst, unsigned long long n, uint64_t s
   }
 }
 
+// One resident wave (4 x 256 threads per SM) with the shared-memory carveout
+// at its maximum, so a counting CTA (96+ KiB of shared memory) can join each
+// SM while the generator still runs: with the PDL trigger at entry, a count
+// launched behind a generator really overlaps it -- the hazard the
+// generate-then-count test needs (an SM can only host CTAs of one carveout).
 static unsigned gen_grid(unsigned long long n) {
+  static bool carveout_set = false;
+  if (!carveout_set) {
+    const void *ks[] = {(const void *)gen_uniform_kernel, (const void *)gen_bernoulli_kernel,
+                        (const void *)gen_blocks_kernel, (const void *)gen_onehot32_kernel,
+                        (const void *)gen_codes8_kernel};
+    for (const void *k : ks)
+      cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
+    cudaGetLastError();
+    carveout_set = true;
+  }
   unsigned long long g = (n + 255) / 256;
-  const unsigned long long cap = 148ull * 16;
+  const unsigned long long cap = 148ull * 4;
   if (g > cap) g = cap;
   return (unsigned)(g ? g : 1);
 }

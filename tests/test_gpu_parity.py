@@ -324,3 +324,29 @@ def test_cuda_graph_capture_and_replay(cuda, oracle, rng):
     g.replay()
     torch.cuda.synchronize()
     assert [int(x) for x in cnt.cpu()] == oracle.hs512(host2, 5, 2 << 20, 16)
+
+
+def test_pdl_contract_generate_then_count(cuda, oracle):
+    """The device generators trigger dependents at entry, so each pp_count
+    (PDL-launched below 512 MiB) may start while its input is still being
+    written; griddepcontrol.wait before the first read must make every
+    count see the complete input."""
+    torch, pp = cuda
+    from paper_2412_16370_b200 import gen
+    n = 64 << 20
+    buf = torch.empty(n, dtype=torch.uint8, device="cuda")
+    cnt = torch.zeros((12, 16), dtype=torch.int64, device="cuda")
+    for i in range(12):  # no host sync in between
+        gen.generate("uniform", n, 1000 + i, out=buf)
+        pp.pospopcnt(buf, 16, counters=cnt[i])
+    codes = torch.empty(n, dtype=torch.uint8, device="cuda")
+    ccnt = torch.zeros((4, 32), dtype=torch.int64, device="cuda")
+    for i in range(4):
+        gen.generate("codes8", n, 2000 + i, out=codes)
+        pp.pospopcnt_categories(codes, 32, counters=ccnt[i])
+    torch.cuda.synchronize()
+    for i in range(12):
+        host = oracle.gen_uniform(n, 1000 + i)
+        assert [int(x) for x in cnt[i].cpu()] == oracle.hs512(host, 0, n, 16, threads=8), i
+    for i in range(4):
+        assert [int(x) for x in ccnt[i].cpu()] == oracle.categories(oracle.gen_codes8(n, 2000 + i), 32)
