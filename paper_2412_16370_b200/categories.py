@@ -15,7 +15,7 @@ w-bit word and are not counted).  Computed by pp_count_categories
 import numpy as np
 
 from . import _lib
-from .core import check_width, is_torch_tensor, new_counters
+from .core import KernelUnavailableError, check_width, is_torch_tensor, new_counters
 from .kernels import _add_into, _device_counters, _device_scratch
 
 _CODE_BYTES = {1: 1, 2: 2, 4: 4}
@@ -31,6 +31,8 @@ def pospopcnt_categories(codes, width, counters=None):
     """
     import torch
     check_width(width)
+    if not torch.cuda.is_available():
+        raise KernelUnavailableError("pospopcnt_categories needs an sm_100 GPU (no CPU fallback)")
     if not is_torch_tensor(codes):
         codes = torch.as_tensor(np.ascontiguousarray(codes)).cuda()
     elif not codes.is_cuda:

@@ -240,3 +240,14 @@ def test_shard_ranges_cover_and_align():
                 assert b == c and a <= b and b % 64 == 0
     with pytest.raises(ValueError):
         shard_range(100, 2, 2)
+
+
+@pytest.mark.skipif(_gpu_present(), reason="checks the no-GPU behaviour")
+def test_categories_and_segments_fail_loudly_without_gpu():
+    import numpy as np
+    with pytest.raises(pp.KernelUnavailableError):
+        pp.pospopcnt_categories(np.zeros(16, dtype=np.uint8), 8)
+    with pytest.raises(ValueError):
+        pp.pospopcnt_categories(np.zeros(16, dtype=np.uint8), 12)
+    with pytest.raises(ValueError):  # segmented counting needs device data
+        pp.pospopcnt_segmented(b"\x00" * 16, [0, 8, 16], 8)
