@@ -601,7 +601,13 @@ static unsigned grid_for(unsigned long long nchunks, unsigned long long cap) {
 // per 1 MiB call, 14.4 -> 10.8 us per 64 MiB, +7 % at 256 MiB, but -1 % at
 // 1 GiB where the overlapping CTAs contend; hence the size cut below.
 // PP_NO_PDL=1 disables it (A/B runs).
-constexpr unsigned long long kPdlMaxBody = 512ull << 20;
+static unsigned long long pdl_max_body() {  // PP_PDL_MAX_MIB overrides (A/B runs)
+  static const unsigned long long v = [] {
+    const char *e = std::getenv("PP_PDL_MAX_MIB");
+    return (e ? std::strtoull(e, nullptr, 10) : 512ull) << 20;
+  }();
+  return v;
+}
 
 template <typename Kern>
 static cudaError_t launch_tma(Kern kernel, unsigned grid, unsigned block, size_t smem,
@@ -627,7 +633,7 @@ cudaError_t launch_count(const CountArgs &a, LoadPath path, const DevInfo &di,
   if (path == LoadPath::kTma) {
     const unsigned g = grid_for(a.nchunks, (unsigned long long)di.num_sms);
     cudaError_t e = launch_tma(pp_tma_kernel<1>, g, kTmaThreads, kTmaSmemBytes, st, a, nullptr,
-                               a.body_bytes < kPdlMaxBody);
+                               a.body_bytes < pdl_max_body());
     if (e != cudaSuccess) return e;
   } else {
     const unsigned g =
@@ -660,7 +666,7 @@ cudaError_t launch_readonly(const CountArgs &a, unsigned long long *sink, const 
                             cudaStream_t st) {
   const unsigned g = grid_for(a.nchunks, (unsigned long long)di.num_sms);
   return launch_tma(pp_tma_kernel<0>, g, kTmaThreads, kTmaSmemBytes, st, a, sink,
-                    a.body_bytes < kPdlMaxBody);
+                    a.body_bytes < pdl_max_body());
 }
 
 cudaError_t launch_segmented(const SegArgs &a, const DevInfo &di, cudaStream_t st) {
