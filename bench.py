@@ -291,6 +291,10 @@ def main_gpu(args):
     # with the allreduce of the counters; plain `python bench.py` is N=1 local
     use_dist = "LOCAL_RANK" in os.environ or world > 1
     if use_dist:
+        # leave 8 SMs to NCCL so each step's allreduce runs concurrently with
+        # the next count (the count is HBM-bound: 140 SMs saturate it)
+        os.environ.setdefault("PP_RESERVE_SMS", "8")
+    if use_dist:
         dist.init_process_group("nccl", device_id=dev)
     lib = _lib.load()
     st = torch.cuda.current_stream(dev)

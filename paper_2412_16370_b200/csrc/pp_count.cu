@@ -583,6 +583,11 @@ cudaError_t device_info(int dev, DevInfo *out) {
       return e;
     if (d.seg_blocks_per_sm < 1) d.seg_blocks_per_sm = 1;
     if (d.ldg_blocks_per_sm < 1) d.ldg_blocks_per_sm = 1;
+    {  // SMs left free for concurrent work (e.g. NCCL kernels of a sharded job)
+      const char *r = std::getenv("PP_RESERVE_SMS");
+      const int reserve = r ? std::atoi(r) : 0;
+      d.count_sms = (reserve > 0 && reserve < d.num_sms) ? d.num_sms - reserve : d.num_sms;
+    }
     d.ready = true;
     cache[dev] = d;
   }
@@ -631,7 +636,7 @@ static cudaError_t launch_tma(Kern kernel, unsigned grid, unsigned block, size_t
 cudaError_t launch_count(const CountArgs &a, LoadPath path, const DevInfo &di,
                          cudaStream_t st) {
   if (path == LoadPath::kTma) {
-    const unsigned g = grid_for(a.nchunks, (unsigned long long)di.num_sms);
+    const unsigned g = grid_for(a.nchunks, (unsigned long long)di.count_sms);
     cudaError_t e = launch_tma(pp_tma_kernel<1>, g, kTmaThreads, kTmaSmemBytes, st, a, nullptr,
                                a.body_bytes < pdl_max_body());
     if (e != cudaSuccess) return e;
@@ -644,7 +649,7 @@ cudaError_t launch_count(const CountArgs &a, LoadPath path, const DevInfo &di,
 }
 
 cudaError_t launch_count_codes8(const CountArgs &a, const DevInfo &di, cudaStream_t st) {
-  const unsigned g = grid_for(a.nchunks, (unsigned long long)di.num_sms);
+  const unsigned g = grid_for(a.nchunks, (unsigned long long)di.count_sms);
   switch (a.width) {
     case 8:
       return launch_tma(pp_tma_kernel<8, PP_CAT_NCW>, g, CatShape::kThreads, CatShape::kSmem, st,
@@ -664,7 +669,7 @@ cudaError_t launch_count_codes8(const CountArgs &a, const DevInfo &di, cudaStrea
 
 cudaError_t launch_readonly(const CountArgs &a, unsigned long long *sink, const DevInfo &di,
                             cudaStream_t st) {
-  const unsigned g = grid_for(a.nchunks, (unsigned long long)di.num_sms);
+  const unsigned g = grid_for(a.nchunks, (unsigned long long)di.count_sms);
   return launch_tma(pp_tma_kernel<0>, g, kTmaThreads, kTmaSmemBytes, st, a, sink,
                     a.body_bytes < pdl_max_body());
 }

@@ -42,6 +42,10 @@ def pospopcnt_sharded(local_data, width, group=None, counters=None, count_fn=Non
     ``counters`` when given).  ``count_fn(data, width, counters_tensor)`` is
     the per-shard counter; it defaults to the sm_100a kernel and exists so
     the collective plumbing can be exercised on CPU with gloo in tests.
+
+    For pipelined jobs (count step i+1 while step i's counters are reduced)
+    set ``PP_RESERVE_SMS=8`` before the first count: the persistent counting
+    grid then leaves SMs to NCCL's kernels at no cost to its HBM-bound rate.
     """
     check_width(width)
     fn = count_fn or _count_cuda
