@@ -466,6 +466,29 @@ def main_gpu(args):
             torch.cuda.synchronize()
             per_width[str(ww)] = round(nbytes * args.steps / (q0.elapsed_time(q1) / 1e3) / 1e9, 1)
 
+    # C4's short / unaligned sweep: device time per call for every length of
+    # BASELINE config 4 at byte offsets 1..7 (latency-bound below ~16 MiB)
+    c4_sweep = None
+    if cfg == "c4":
+        c4_sweep = {}
+        scratch_c = torch.zeros(64, dtype=torch.int64, device=dev)
+        for words in (1, 3, 17, 255, 512, 8192, 131072, 8388608):
+            nb = 8 * words
+            reps = 200 if nb <= (1 << 20) else 50
+            for _ in range(5):
+                _lib.check(lib.pp_count(buf.data_ptr() + 1, nb, 64, scratch_c.data_ptr(), sp))
+            gpu_busy()
+            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            q0.record(st)
+            for r in range(reps):
+                off = 1 + r % 7
+                _lib.check(lib.pp_count(buf.data_ptr() + off, nb, 64, scratch_c.data_ptr(), sp))
+            q1.record(st)
+            torch.cuda.synchronize()
+            us = q0.elapsed_time(q1) / reps * 1e3
+            c4_sweep[str(words)] = {"us_per_call": round(us, 2),
+                                    "GBs": round(nb / us / 1e3, 2)}
+
     # the paper's read-only "roofline" kernel over the same bytes
     sink = torch.zeros(1, dtype=torch.int64, device=dev)
     for _ in range(max(3, args.warmup)):
@@ -562,6 +585,7 @@ def main_gpu(args):
             "clocks": clk.summary(),
             "exact": exact,
             "per_width_gbs": per_width,
+            "c4_short_sweep": c4_sweep,
         }
         print(json.dumps(line), flush=True)
     if use_dist:
