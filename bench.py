@@ -330,6 +330,16 @@ def main_gpu(args):
     # waits), and the timed region waits for every exchange (drain()).
     counters2 = torch.zeros((2, 64), dtype=torch.int64, device=dev)
     counters = counters2[0]
+    # --exchange fused (default under torchrun for the plain count): no
+    # collective per step; each rank's kernel adds every CTA's counts into all
+    # ranks' IPC-mapped counters (pp_count_multi), so a step ends when the
+    # kernel does and the max over ranks of the event timings covers it
+    fused = use_dist and args.exchange == "fused" and not categorical and cfg != "c4seg"
+    peers = None
+    if fused:
+        from paper_2412_16370_b200.dist import PeerCounters
+        peers = PeerCounters(device=dev)
+        ntgt = len(peers.targets)
     globs = [torch.zeros(64, dtype=torch.int64, device=dev) for _ in range(2)]
     count_ev = [torch.cuda.Event() for _ in range(2)]
     snap_ev = [torch.cuda.Event() for _ in range(2)]
@@ -348,6 +358,10 @@ def main_gpu(args):
             _lib.check(lib.pp_count_fixed(view_ptr, 4096, nbytes // 4096, w, seg_out.data_ptr(),
                                           _lib.PP_SEG_OVERWRITE, sp))
         else:
+            if fused:
+                _lib.check(lib.pp_count_multi(view_ptr, nbytes, w, peers.targets, ntgt, sp))
+                nstep[0] += 1
+                return
             if use_dist:
                 st.wait_event(snap_ev[b])  # step i-2's snapshot of counters2[b] is taken
             if categorical:  # one u8 code per byte
@@ -367,7 +381,7 @@ def main_gpu(args):
         nstep[0] += 1
 
     def drain():
-        if use_dist:  # the last exchanges complete inside the timed region
+        if use_dist and not fused:  # the last exchanges complete inside the timed region
             st.wait_event(red_ev[0])
             st.wait_event(red_ev[1])
 
@@ -394,7 +408,7 @@ def main_gpu(args):
         dist.barrier()
     torch.cuda.synchronize()
     t_ms = e0.elapsed_time(e1)
-    if not use_dist:
+    if not use_dist or fused:
         # each step is exactly one launch of the dominant kernel
         k_ms = t_ms / args.steps
     else:
@@ -425,7 +439,7 @@ def main_gpu(args):
     exact = None
     if args.check and cfg == "c5" and rank == 0:
         want = golden_total("c5_w16_64gib_total")
-        src = (globs[0] + globs[1]) if use_dist else counters2.sum(0)
+        src = peers.local if fused else (globs[0] + globs[1]) if use_dist else counters2.sum(0)
         got = src.cpu().numpy().view(np.uint64)[:w]
         total = args.warmup + args.steps
         exact = None if want is None else bool(
@@ -437,6 +451,21 @@ def main_gpu(args):
         got = counters2.sum(0).cpu().numpy().view(np.uint64)[:w]
         total = args.warmup + args.steps
         exact = bool(all(int(g) == total * x for g, x in zip(got, want)))
+    elif args.check and fused and cfg in ("c1", "c2", "c3", "c4"):
+        # every rank's oracle on its own shard, summed over ranks, against the
+        # job total the fused exchange left in this rank's counters
+        from oracle import oracle as O
+        host = buf.cpu().numpy()
+        want = torch.tensor(O.hs512(host, offset, nbytes, w,
+                                    threads=max(1, host_threads() // world)),
+                            dtype=torch.int64, device=dev)
+        del host
+        dist.all_reduce(want)
+        total = args.warmup + args.steps
+        ok = torch.tensor([int(bool(torch.equal(peers.local[:w], total * want)))],
+                          dtype=torch.int64, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        exact = bool(ok.item())
     elif args.check and cfg in ("c1", "c2", "c3", "c4") and rank == 0:
         from oracle import oracle as O
         host = buf.cpu().numpy()
@@ -569,14 +598,18 @@ def main_gpu(args):
             "config": {"workload": desc, "word_width": w,
                        "bytes_per_gpu_per_step": per_step_bytes,
                        "bytes_per_step_all_gpus": job_bytes,
-                       "parallelism": f"dp{world} (contiguous shards, NCCL allreduce of "
-                                      f"{w} counters per step)" if world > 1 else "single GPU",
+                       "parallelism": (f"dp{world} (shards; fused exchange: the counting "
+                                       "kernel adds into every rank's IPC-mapped counters)"
+                                       if fused else
+                                       f"dp{world} (shards, NCCL allreduce of {w} counters "
+                                       "per step)") if world > 1 else "single GPU",
                        "l2": "input >> 126 MB L2, no flush needed" if nbytes > 256 * MIB
                              else "input fits L2 (reported, not judged vs HBM)"},
             "hbm_frac": round(value / world / peak, 4),
             "exact_reference": "C5: reference numba total of the 64 GiB array (golden.json)"
                                if cfg == "c5" else "CPU oracle (C port of NumbaKernel.run) "
-                                                   "on rank 0's shard",
+                                                   + ("of every rank's shard, summed" if fused
+                                                      else "on rank 0's shard"),
             "words_per_s": round(value * 1e9 / (w // 8)),
             "roofline": roofline,
             "cpu_baseline": cpu,
@@ -588,6 +621,9 @@ def main_gpu(args):
             "c4_short_sweep": c4_sweep,
         }
         print(json.dumps(line), flush=True)
+    if peers is not None:
+        peers.sync()
+        peers.close()
     if use_dist:
         dist.destroy_process_group()
     return 0
@@ -601,6 +637,8 @@ def main():
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--config", choices=tuple(CONFIGS), default="c2")
     ap.add_argument("--width", type=int, default=0, help="override w for c2 (sweep)")
+    ap.add_argument("--exchange", choices=("fused", "nccl"), default="fused",
+                    help="N>1 counter exchange: in-kernel remote adds, or NCCL allreduce")
     ap.add_argument("--no-check", dest="check", action="store_false")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")

@@ -107,6 +107,29 @@ PP_API int pp_count_fixed(const void *base, size_t seg_bytes, size_t nseg, int w
                    unsigned long long *out, int flags, void *stream);
 
 /*
+ * pp_count_multi — pp_count whose result is added into EVERY target counter
+ * array: the sharded job's allreduce fused into the counting kernel.  Each
+ * CTA adds its folded counts into targets[0..ntargets-1] with u64 atomics;
+ * targets may be peer-mapped device memory (other ranks' counters opened
+ * with pp_ipc_open), i.e. remote atomics over NVLink.  When every rank has
+ * run pp_count_multi over its shard with the same target set and the kernels
+ * completed, every rank's counters hold the job total -- no NCCL call.
+ * Replaces: the per-shard Kernel.run (kernels.py:242-270) + the combine of
+ * the shard counters (additivity).  ntargets <= PP_MAX_TARGETS.
+ */
+#define PP_MAX_TARGETS 16
+PP_API int pp_count_multi(const void *data, size_t nbytes, int width,
+                          unsigned long long *const *targets, int ntargets, void *stream);
+
+/* CUDA IPC for the targets of pp_count_multi (one process per GPU): export a
+ * device allocation as a 64-byte handle, open a peer's handle (peer access
+ * is enabled lazily), close it again. */
+#define PP_IPC_HANDLE_BYTES 64
+PP_API int pp_ipc_handle(const void *dev_ptr, void *handle64);
+PP_API int pp_ipc_open(const void *handle64, void **dev_ptr);
+PP_API int pp_ipc_close(void *dev_ptr);
+
+/*
  * pp_count_frame — one pass for every word width:
  * frame64[i] += #{set bits b of bytes at address A : 8*(A mod 8) + b == i}
  * over the device bytes [data, data+nbytes) (any length, any alignment).

@@ -18,6 +18,8 @@ LIB_PATH = os.environ.get("PP_LIB_PATH") or os.path.join(HERE, "libpospopcnt_b20
 
 PP_OK, PP_EWIDTH, PP_ELENGTH, PP_ECUDA, PP_EARG, PP_ENODEV = range(6)
 PP_SEG_ACCUMULATE, PP_SEG_OVERWRITE = 0, 1
+PP_MAX_TARGETS = 16        # pp_count_multi: counter arrays per call
+PP_IPC_HANDLE_BYTES = 64   # pp_ipc_handle: opaque handle size
 ABI_VERSION = 1
 
 # name -> (restype, argtypes); mirrors include/pospopcnt_b200.h
@@ -31,6 +33,10 @@ SIGNATURES = {
     "pp_count": (_int, [_vp, _sz, _int, _vp, _vp]),
     "pp_count_host": (_int, [_vp, _sz, _int, _vp]),
     "pp_count_frame": (_int, [_vp, _sz, _vp, _vp]),
+    "pp_count_multi": (_int, [_vp, _sz, _int, _vp, _int, _vp]),
+    "pp_ipc_handle": (_int, [_vp, _vp]),
+    "pp_ipc_open": (_int, [_vp, _vp]),
+    "pp_ipc_close": (_int, [_vp]),
     "pp_count_categories": (_int, [_vp, _sz, _int, _int, _vp, _vp]),
     "pp_count_segmented": (_int, [_vp, _vp, _sz, _int, _vp, _int, _vp]),
     "pp_count_fixed": (_int, [_vp, _sz, _sz, _int, _vp, _int, _vp]),

@@ -142,6 +142,58 @@ int pp_count_frame(const void *data, size_t nbytes, unsigned long long *frame64,
   return count_device(data, nbytes, 64, frame64, static_cast<cudaStream_t>(stream), di, true);
 }
 
+int pp_count_multi(const void *data, size_t nbytes, int width,
+                   unsigned long long *const *targets, int ntargets, void *stream) {
+  if (!width_ok(width)) return fail(PP_EWIDTH, "word width must be one of (8, 16, 32, 64), got %d", width);
+  if (nbytes % (size_t)(width / 8))
+    return fail(PP_ELENGTH, "%zu bytes is not a multiple of the %d-byte word size", nbytes,
+                width / 8);
+  if (!targets || ntargets < 1 || ntargets > PP_MAX_TARGETS)
+    return fail(PP_EARG, "need 1..%d target counter arrays, got %d", PP_MAX_TARGETS, ntargets);
+  int rc;
+  for (int k = 0; k < ntargets; ++k)
+    if ((rc = check_device_ptr(targets[k], "targets[k]"))) return rc;
+  if (nbytes == 0) return PP_OK;
+  if ((rc = check_device_ptr(data, "data"))) return rc;
+  pp::DevInfo di;
+  if ((rc = current_devinfo(&di))) return rc;
+  pp::CountArgs a{};
+  const pp::LoadPath path = load_path();
+  pp::split_range(static_cast<const uint8_t *>(data), nbytes, pp::count_chunk_bytes(path), &a);
+  a.counters = targets[0];
+  a.width = width;
+  a.nextra = ntargets - 1;
+  for (int k = 1; k < ntargets; ++k) a.extra[k - 1] = targets[k];
+  cudaError_t e = pp::launch_count(a, path, di, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "pp_count_multi launch");
+  return PP_OK;
+}
+
+int pp_ipc_handle(const void *dev_ptr, void *handle64) {
+  if (!dev_ptr || !handle64) return fail(PP_EARG, "NULL argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == PP_IPC_HANDLE_BYTES, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void *>(dev_ptr));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  std::memcpy(handle64, &h, sizeof h);
+  return PP_OK;
+}
+
+int pp_ipc_open(const void *handle64, void **dev_ptr) {
+  if (!handle64 || !dev_ptr) return fail(PP_EARG, "NULL argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof h);
+  cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  return PP_OK;
+}
+
+int pp_ipc_close(void *dev_ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
+  return PP_OK;
+}
+
 int pp_count_categories(const void *codes, size_t ncodes, int code_bytes, int width,
                         unsigned long long *counters, void *stream) {
   if (!width_ok(width)) return fail(PP_EWIDTH, "word width must be one of (8, 16, 32, 64), got %d", width);

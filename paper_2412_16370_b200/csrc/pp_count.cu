@@ -78,18 +78,23 @@ __device__ __forceinline__ void count_edges(Counter &c, const uint8_t *head, uin
 }
 
 // counters[j] += sum_{i = j mod w} frame[(i + rot) mod 64]   (flush_fw)
+// With pp_count_multi the same sums also go to a.extra[] -- typically the
+// other ranks' counters mapped over NVLink, so these atomics ARE the sharded
+// job's allreduce, fused into the counting kernel (remote RED.ADD.64).
 __device__ __forceinline__ void fold_frame_to_counters(const unsigned long long *frame,
-                                                       unsigned long long *counters,
-                                                       int width, int rot) {
-  int j = threadIdx.x;
+                                                       const CountArgs &a) {
+  const int j = threadIdx.x, width = a.width;
   if (j < width) {
     // under programmatic dependent launch the previous grid on the stream may
     // still be running: its counter updates complete before ours (no-op
     // without PDL)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     unsigned long long s = 0;
-    for (int i = j; i < 64; i += width) s += frame[(i + rot) & 63];
-    if (s) atomicAdd(counters + j, s);
+    for (int i = j; i < 64; i += width) s += frame[(i + a.rot) & 63];
+    if (s) {
+      atomicAdd(a.counters + j, s);
+      for (int k = 0; k < a.nextra; ++k) atomicAdd(a.extra[k] + j, s);
+    }
   }
 }
 
@@ -339,7 +344,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     }
   }
   __syncthreads();
-  if (kCount) fold_frame_to_counters(frame, a.counters, a.width, a.rot);
+  if (kCount) fold_frame_to_counters(frame, a);
 }
 
 __global__ void __launch_bounds__(kLdgThreads)
@@ -374,7 +379,7 @@ __global__ void __launch_bounds__(kLdgThreads)
   atomicAdd(&frame[lane], c.ce);
   atomicAdd(&frame[32 + lane], c.co);
   __syncthreads();
-  fold_frame_to_counters(frame, a.counters, a.width, a.rot);
+  fold_frame_to_counters(frame, a);
 }
 
 // Bytes [max(va, lo), min(va + 16, hi)) of the aligned 16-byte block at va,

@@ -20,6 +20,10 @@ struct CountArgs {
   unsigned long long *counters;
   int width;
   int rot;  // 8 * (address of first byte mod 8), flush_fw's rot (accumulate.py:115-130)
+  // pp_count_multi: further counter arrays (often peer-mapped over NVLink)
+  // that receive the same counts as `counters`
+  int nextra;
+  unsigned long long *extra[15];
 };
 
 struct SegArgs {

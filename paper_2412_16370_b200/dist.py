@@ -1,18 +1,33 @@
-"""Multi-GPU sharding: one process per GPU, counters combined by one allreduce.
+"""Multi-GPU sharding: one process per GPU, one exchange of <= 64 counters.
 
 The reference is single-threaded by design; counts are
 additive over word-complete splits (pkg/tests/test_acceptance.py:
 196-204), so a P-way data-parallel count is: contiguous shards cut at
 multiples of lcm(16, w/8) bytes, each rank counting its own shard with the
-sm_100a kernel, then one ``all_reduce(SUM)`` of the w counters.  Over NCCL on
-NVLink/NVSwitch that message is <= 64 x 8 B: latency-bound, a few microseconds.
+sm_100a kernel, then one sum of the w counters over the ranks.
+
+Two ways to do the sum:
+
+* ``PeerCounters`` (the product path): every rank maps every other rank's
+  counter array into its address space once (CUDA IPC; peer access over
+  NVLink/NVSwitch), and the counting kernel's epilogue adds each CTA's folded
+  counts into ALL ranks' arrays with u64 atomics (``pp_count_multi``).  The
+  allreduce is fused into the counting kernel: no collective call per count,
+  the exchange overlaps the other CTAs' streaming, and after a barrier every
+  rank holds the job total.
+* ``all_reduce`` of an int64 tensor over the process group (NCCL, or gloo on
+  CPU): the baseline, also what the CPU tests exercise.
+
 Counters travel as int64 (identical bits to u64 addition mod 2^64).
 """
+
+import ctypes
 
 import torch
 import torch.distributed as dist
 
-from .core import check_width
+from . import _lib
+from .core import W_MAX, check_width
 
 SHARD_ALIGN = 64  # multiple of 16 (vector) and of every word size
 
@@ -29,25 +44,112 @@ def shard_range(total_bytes, world, rank, align=SHARD_ALIGN):
     return lo, hi
 
 
+class PeerCounters:
+    """Every rank's 64 counters, mapped into this process (CUDA IPC).
+
+    Collective constructor: every rank of ``group`` must create one (on its
+    own device).  ``local`` is this rank's int64[64] counter tensor; after
+    every rank has run ``count`` over its shard and ``sync()`` has returned,
+    ``local`` holds the sum over all ranks' shards.
+    """
+
+    def __init__(self, group=None, device=None):
+        self.lib = _lib.load()
+        self.group = group
+        self.device = torch.device(device) if device is not None else \
+            torch.device("cuda", torch.cuda.current_device())
+        self.local = torch.zeros(W_MAX, dtype=torch.int64, device=self.device)
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        if self.world > _lib.PP_MAX_TARGETS:
+            raise ValueError(f"at most {_lib.PP_MAX_TARGETS} ranks per fused exchange")
+        handle = ctypes.create_string_buffer(_lib.PP_IPC_HANDLE_BYTES)
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.pp_ipc_handle(self.local.data_ptr(), handle))
+        handles = [handle.raw]
+        if self.world > 1:
+            handles = [None] * self.world
+            dist.all_gather_object(handles, handle.raw, group=group)
+        self._opened = []
+        ptrs = []
+        with torch.cuda.device(self.device):
+            for r, h in enumerate(handles):
+                if r == self.rank:
+                    ptrs.append(self.local.data_ptr())
+                    continue
+                p = ctypes.c_void_p()
+                _lib.check(self.lib.pp_ipc_open(ctypes.create_string_buffer(h, len(h)),
+                                                ctypes.byref(p)))
+                self._opened.append(p.value)
+                ptrs.append(p.value)
+        # own array first: it is the kernel's primary target
+        ptrs.insert(0, ptrs.pop(self.rank))
+        self.targets = (ctypes.c_void_p * len(ptrs))(*ptrs)
+        self.sync()
+
+    def count(self, data, nbytes, width, stream=None):
+        """Count device bytes [data, data+nbytes) into every rank's counters."""
+        st = torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream
+        _lib.check(self.lib.pp_count_multi(ctypes.c_void_p(data), nbytes, width, self.targets,
+                                           len(self.targets), ctypes.c_void_p(st)))
+
+    def zero(self):
+        """Reset the job counters (collective: all ranks, before counting)."""
+        self.local.zero_()
+        self.sync()
+
+    def sync(self):
+        """Wait until every rank's pending counts (and so all its remote adds)
+        have completed: local device sync + a barrier over the group."""
+        torch.cuda.synchronize(self.device)
+        if self.world > 1:
+            dist.barrier(group=self.group)
+
+    def close(self):
+        for p in self._opened:
+            self.lib.pp_ipc_close(ctypes.c_void_p(p))
+        self._opened = []
+
+
 def _count_cuda(data, width, counters):
     from .kernels import pospopcnt
     return pospopcnt(data, width, counters=counters)
 
 
-def pospopcnt_sharded(local_data, width, group=None, counters=None, count_fn=None):
-    """Count this rank's shard and allreduce the counters over ``group``.
+def pospopcnt_sharded(local_data, width, group=None, counters=None, count_fn=None,
+                      peers=None):
+    """Count this rank's shard and combine the counters over ``group``.
 
     ``local_data`` is this rank's (word-complete) shard.  Returns an int64
     tensor of ``width`` global counters on the shard's device (added into
-    ``counters`` when given).  ``count_fn(data, width, counters_tensor)`` is
-    the per-shard counter; it defaults to the sm_100a kernel and exists so
-    the collective plumbing can be exercised on CPU with gloo in tests.
+    ``counters`` when given).
 
-    For pipelined jobs (count step i+1 while step i's counters are reduced)
-    set ``PP_RESERVE_SMS=8`` before the first count: the persistent counting
-    grid then leaves SMs to NCCL's kernels at no cost to its HBM-bound rate.
+    With ``peers`` (a ``PeerCounters``) the combine is fused into the
+    counting kernel (remote atomics into every rank's counters over NVLink)
+    and only a barrier follows; ``peers.local`` accumulates across calls.
+    Otherwise the shard is counted into a fresh tensor and all-reduced over
+    the group (NCCL, or gloo for CPU tensors).  ``count_fn(data, width,
+    counters_tensor)`` replaces the per-shard counter in that path; it exists
+    so the collective plumbing can be exercised on CPU with gloo in tests.
+
+    Pipelined NCCL jobs (count step i+1 while step i's counters are reduced)
+    should set ``PP_RESERVE_SMS=8`` before the first count: the persistent
+    counting grid then leaves SMs to NCCL's kernels at no cost to its
+    HBM-bound rate.
     """
     check_width(width)
+    if peers is not None:
+        from .core import InputView
+        view = InputView.of(local_data).check_complete(width)
+        if not view.on_device:
+            raise ValueError("the fused exchange needs the shard in device memory")
+        peers.count(view.base.data_ptr() + view.offset, view.nbytes, width)
+        peers.sync()
+        out = peers.local[:width]
+        if counters is not None:
+            counters[:width] += out.to(counters.device, counters.dtype)
+            return counters
+        return out.clone()
     fn = count_fn or _count_cuda
     dev = local_data.device if hasattr(local_data, "device") else torch.device("cpu")
     local = torch.zeros(width, dtype=torch.int64, device=dev)
