@@ -534,7 +534,8 @@ def main_gpu(args):
 
     peak, peak_src = load_peaks()
     achieved = per_step_bytes / (k_ms / 1e3) / 1e9
-    kernel_key = ("pp_seg_kernel" if seg_out is not None else
+    seg_tma = os.environ.get("PP_SEG_PATH", "") != "ldg" and view_ptr % 16 == 0
+    kernel_key = (("pp_segtma_kernel<8>" if seg_tma else "pp_seg_kernel") if seg_out is not None else
                   "pp_cat_kernel<1>" if categorical else "pp_tma_kernel<1>")
     traffic, traffic_ratio = load_traffic(kernel_key, per_step_bytes)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

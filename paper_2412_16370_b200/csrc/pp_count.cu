@@ -18,6 +18,7 @@
 //
 // Segmented mode: pp_seg_kernel<G>, G lanes per segment.
 #include <cstdlib>
+#include <cstring>
 
 #include "pp_device.cuh"
 #include "pp_internal.h"
@@ -538,6 +539,125 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
   }
 }
 
+// Fixed-size segments (pp_count_fixed) fed by a CTA-wide TMA ring.  A chunk
+// is k whole "items" of S = 32/G consecutive segments (one warp's worth), so
+// no segment straddles a stage.  The 8 consumer warps form two teams of 4;
+// team q consumes this CTA's chunks j = q (mod 2), each warp taking items
+// wi, wi + 4, ... of the chunk.  Chunk j uses stage j mod 2, so each stage
+// belongs to one team and is consumed in order (an mbarrier parity wait is
+// only sound when the waiter is at most one phase ahead).  Lanes
+// read their segment's vectors from shared memory (a quarter/half/whole warp
+// reads 128/256/512 contiguous bytes: conflict-free), count with the same
+// G-lane carry-save counter as pp_seg_kernel and write the row.  Requires a
+// 16-byte aligned base, seg_bytes % 16 == 0 and S * seg_bytes <= 16 KiB.
+#ifndef PP_SEGTMA_EARLY_RELEASE
+#define PP_SEGTMA_EARLY_RELEASE 1
+#endif
+#ifndef PP_SEGTMA_TEAMS  // A/B knobs (scripts/gpu_segtma.sh)
+#define PP_SEGTMA_TEAMS 2
+#define PP_SEGTMA_TEAM_WARPS 4
+#define PP_SEGTMA_STAGES 2
+#define PP_SEGTMA_STAGE_KIB 64
+#endif
+constexpr int kSegTmaTeams = PP_SEGTMA_TEAMS, kSegTmaTeamWarps = PP_SEGTMA_TEAM_WARPS;
+constexpr int kSegTmaWarps = kSegTmaTeams * kSegTmaTeamWarps, kSegTmaStages = PP_SEGTMA_STAGES;
+constexpr unsigned kSegTmaStageBytes = PP_SEGTMA_STAGE_KIB << 10;
+static_assert(kSegTmaStages % kSegTmaTeams == 0, "each stage must belong to one team");
+constexpr int kSegTmaThreads = (kSegTmaWarps + 1) * 32;
+constexpr size_t kSegTmaSmem = kSegTmaStages * (size_t)kSegTmaStageBytes + 2 * kSegTmaStages * 8;
+
+template <int G>
+__global__ void __launch_bounds__(kSegTmaThreads, 1)
+    pp_segtma_kernel(SegArgs a, unsigned items_per_chunk) {
+  constexpr int S = 32 / G;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint4 *stages = reinterpret_cast<uint4 *>(smem);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kSegTmaStages * kSegTmaStageBytes);
+  uint64_t *empty = full + kSegTmaStages;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSegTmaStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kSegTmaTeamWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const unsigned long long seg_bytes = a.seg_bytes, nseg = a.nseg;
+  const unsigned long long segs_per_chunk = (unsigned long long)items_per_chunk * S;
+  const unsigned long long chunk_bytes = segs_per_chunk * seg_bytes;
+  const unsigned long long total = nseg * seg_bytes;
+  const unsigned long long nchunks = (nseg + segs_per_chunk - 1) / segs_per_chunk;
+  constexpr uint32_t kStageVecs = kSegTmaStageBytes / 16;
+
+  if (warp == kSegTmaWarps) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      uint32_t j = 0;
+      for (unsigned long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x, ++j) {
+        const uint32_t stage = j % kSegTmaStages;
+        mbar_wait(&empty[stage], ((j / kSegTmaStages) & 1u) ^ 1u);
+        const unsigned long long off = ch * chunk_bytes;
+        const unsigned long long rem = total - off;
+        const uint32_t bytes = (uint32_t)(rem < chunk_bytes ? rem : chunk_bytes);
+        mbar_arrive_expect_tx(&full[stage], bytes);
+        bulk_g2s(stages + stage * kStageVecs, a.base + off, bytes, &full[stage], pol);
+      }
+    }
+    return;
+  }
+
+  const uint32_t team = warp / kSegTmaTeamWarps, wi = warp % kSegTmaTeamWarps;
+  const uint32_t r = lane % G, sl = lane / G;
+  const uint32_t segv = (uint32_t)(seg_bytes >> 4);  // vectors per segment
+  const TC t = make_tc(lane);
+  uint32_t j = team;
+  for (unsigned long long ch = blockIdx.x + (unsigned long long)team * gridDim.x; ch < nchunks;
+       ch += (unsigned long long)kSegTmaTeams * gridDim.x, j += kSegTmaTeams) {
+    const uint32_t stage = j % kSegTmaStages;
+    mbar_wait(&full[stage], (j / kSegTmaStages) & 1u);
+    const uint4 *sv = stages + stage * kStageVecs;
+    const unsigned long long seg0 = ch * segs_per_chunk;
+    bool released = false;
+    for (uint32_t it = wi; it < items_per_chunk; it += kSegTmaTeamWarps) {
+      const unsigned long long s = seg0 + (unsigned long long)it * S + sl;
+      if (seg0 + (unsigned long long)it * S >= nseg) break;  // warp-uniform
+      const bool item_full = seg0 + (unsigned long long)(it + 1) * S <= nseg;
+      const uint4 *sp = sv + (it * S + sl) * segv + r;
+      GroupCounter<G, false> c;
+      c.init();
+      for (uint32_t k0 = 0; k0 < segv; k0 += 8 * G) {
+        uint4 v[8];
+        if (item_full && k0 + 8 * G <= segv) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[q] = sp[k0 + q * G];
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const uint32_t k = k0 + q * G + r;
+            v[q] = (k < segv && s < nseg) ? sp[k0 + q * G] : make_uint4(0u, 0u, 0u, 0u);
+          }
+        }
+        c.eat8(v, t);
+      }
+      if (PP_SEGTMA_EARLY_RELEASE && it + kSegTmaTeamWarps >= items_per_chunk) {
+        // this warp's last read of the stage is done: release it before the
+        // flush and the row stores
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        released = true;
+      }
+      c.finish(t);
+      if (s < nseg) write_row(a, s, reinterpret_cast<uintptr_t>(a.base) + s * seg_bytes, c, lane);
+    }
+    if (!released) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ host side
 void split_range(const uint8_t *data, unsigned long long nbytes,
                  unsigned long long chunk_bytes, CountArgs *a) {
@@ -579,6 +699,10 @@ cudaError_t device_info(int dev, DevInfo *out) {
                    pp_tma_kernel<32, PP_CAT_NCW>, pp_tma_kernel<64, PP_CAT_NCW>})
       if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)CatShape::kSmem)))
+        return e;
+    for (auto k : {pp_segtma_kernel<8>, pp_segtma_kernel<16>, pp_segtma_kernel<32>})
+      if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kSegTmaSmem)))
         return e;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.seg_blocks_per_sm,
                                                            pp_seg_kernel<8>, kSegThreads, 0)))
@@ -679,9 +803,43 @@ cudaError_t launch_readonly(const CountArgs &a, unsigned long long *sink, const 
                     a.body_bytes < pdl_max_body());
 }
 
+// Fixed segments take the TMA ring when they tile its 64 KiB stages into at
+// least one item per team warp and there are enough chunks to fill the grid;
+// PP_SEG_PATH=ldg forces pp_seg_kernel (A/B runs, tests).
+static bool seg_use_tma(const SegArgs &a, const DevInfo &di, unsigned *items_per_chunk) {
+  static const char *path = std::getenv("PP_SEG_PATH");
+  if (path && std::strcmp(path, "ldg") == 0) return false;
+  const bool force = path && std::strcmp(path, "tma") == 0;
+  if (a.seg_off || a.seg_bytes == 0 || (a.seg_bytes & 15) || ((uintptr_t)a.base & 15)) return false;
+  const unsigned long long item = (unsigned long long)(32 / a.lanes_per_segment) * a.seg_bytes;
+  const unsigned long long k = kSegTmaStageBytes / item;
+  if (k < (unsigned long long)kSegTmaTeamWarps) return false;
+  // >= 32 vectors per lane per segment: below that the per-segment flush
+  // dominates and the LDG kernel's 24 warps/SM hide it better
+  // (scripts/seg_sweep.py, profiles/r1_segmented_ablation.md)
+  if (!force && a.seg_bytes < 512ull * a.lanes_per_segment) return false;
+  const unsigned long long chunks = (a.nseg * a.seg_bytes + k * item - 1) / (k * item);
+  if (!force && chunks < 4ull * di.num_sms) return false;  // small batches: LDG latency wins
+  *items_per_chunk = (unsigned)k;
+  return true;
+}
+
 cudaError_t launch_segmented(const SegArgs &a, const DevInfo &di, cudaStream_t st) {
   if (a.nseg == 0) return cudaSuccess;
   const int G = a.lanes_per_segment;
+  unsigned ipc = 0;
+  if (seg_use_tma(a, di, &ipc)) {
+    const unsigned long long chunks =
+        (a.nseg + (unsigned long long)ipc * (32 / G) - 1) / ((unsigned long long)ipc * (32 / G));
+    const unsigned g = grid_for(chunks, (unsigned long long)di.num_sms);
+    if (G == 8)
+      pp_segtma_kernel<8><<<g, kSegTmaThreads, kSegTmaSmem, st>>>(a, ipc);
+    else if (G == 16)
+      pp_segtma_kernel<16><<<g, kSegTmaThreads, kSegTmaSmem, st>>>(a, ipc);
+    else
+      pp_segtma_kernel<32><<<g, kSegTmaThreads, kSegTmaSmem, st>>>(a, ipc);
+    return cudaGetLastError();
+  }
   const unsigned long long segs_per_block = (kSegThreads / 32) * (32 / G);
   const unsigned long long need = (a.nseg + segs_per_block - 1) / segs_per_block;
   const unsigned g = grid_for(need, (unsigned long long)di.num_sms * di.seg_blocks_per_sm);

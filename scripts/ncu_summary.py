@@ -38,7 +38,7 @@ def short(name):
     for k in ("pp_tma_kernel<32, 16>", "pp_tma_kernel<8, 16>", "pp_tma_kernel<16, 16>",
               "pp_tma_kernel<64, 16>", "pp_tma_kernel<1,", "pp_tma_kernel<0,",
               "pp_tma_kernel<1>", "pp_tma_kernel<0>", "pp_tma_kernel<true>", "pp_tma_kernel<false>",
-              "pp_seg_kernel<8>", "pp_seg_kernel", "pp_cat_kernel<1>", "pp_count_ldg_kernel", "gen_"):
+              "pp_segtma_kernel<8>", "pp_seg_kernel<8>", "pp_seg_kernel", "pp_cat_kernel<1>", "pp_count_ldg_kernel", "gen_"):
         if k in name:
             return {"pp_tma_kernel<true>": "pp_tma_kernel<1>", "pp_tma_kernel<1,": "pp_tma_kernel<1>",
                     "pp_tma_kernel<false>": "pp_tma_kernel<0>", "pp_tma_kernel<0,": "pp_tma_kernel<0>",
