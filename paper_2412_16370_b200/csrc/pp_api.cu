@@ -49,6 +49,11 @@ pp::LoadPath load_path() {
 int current_devinfo(pp::DevInfo *di) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) {
+    cudaGetLastError();
+    // the reference's KernelUnavailableError (core.py:23-28), not a CUDA fault
+    return fail(PP_ENODEV, "no CUDA device: %s", cudaGetErrorString(e));
+  }
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
   e = pp::device_info(dev, di);
   if (e != cudaSuccess) return cuda_fail(e, "device_info");

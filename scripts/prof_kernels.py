@@ -42,8 +42,8 @@ def main():
         if "seg" in which:
             _lib.check(lib.pp_count_fixed(seg_buf.data_ptr(), 4096, n // 4096, 64,
                                           out.data_ptr(), _lib.PP_SEG_OVERWRITE, sp))
-        if "cat" in which:  # one-hot path (w=32) and histogram path (w=64)
-            for w in (32, 64):
+        if "cat" in which:  # fused one-hot producer at every width (u8 codes)
+            for w in (8, 16, 32, 64):
                 _lib.check(lib.pp_count_categories(codes.data_ptr(), n, 1, w, cnt.data_ptr(), sp))
     torch.cuda.synchronize()
     print("ok", [int(x) for x in cnt[:args.width].cpu()][:4])
