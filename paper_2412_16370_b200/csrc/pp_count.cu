@@ -121,6 +121,36 @@ __device__ __forceinline__ uint32_t onehot8x4(uint32_t x, bool any_big) {
   }
   return oh;
 }
+#ifndef PP_CAT_V2
+#define PP_CAT_V2 1
+#endif
+// v2 of the same: 2 ops for the nibble-packed selector (the LOP3 select
+// leaves junk only in the nibbles of codes >= 8, which the mask clears), and
+// a 5-op mask: z = (x | 0x80..) - 0x08.. has a byte's msb set iff that byte
+// is in [8, 0x80) (no borrow crosses a byte), x's msb covers [0x80, 0xFF];
+// PRMT's sign-replicate mode (selector nibble 8|i) widens msb -> 0xFF.
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
+  return d;
+}
+__device__ __forceinline__ uint32_t onehot8x4_v2(uint32_t x, bool any_big) {
+  uint32_t tt;  // (x & 0x07070707) | ((x >> 4) & ~0x07070707): one LOP3
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(tt) : "r"(x), "r"(x >> 4), "r"(0x07070707u));
+  const uint32_t sel = prmt(tt, 0u, 0x0020u);  // nibbles: code0..code3 (low 16 bits)
+  uint32_t oh = prmt(0x08040201u, 0x80402010u, sel);  // junk nibbles: masked below
+  if (any_big) {
+    const uint32_t z = (x | 0x80808080u) - 0x08080808u;
+    oh &= ~prmt(z | x, 0u, 0xBA98u);
+  }
+  return oh;
+}
+// (1 << c) as a (lo, hi) pair; c >= 64 gives 0 (shl.b64 clamps)
+__device__ __forceinline__ void onehot64(uint32_t c, uint32_t &lo, uint32_t &hi) {
+  asm("{\n\t.reg .b64 t;\n\tmov.b64 t, 1;\n\tshl.b64 t, t, %2;\n\tmov.b64 {%0, %1}, t;\n\t}"
+      : "=r"(lo), "=r"(hi) : "r"(c));
+}
+
 // byte k of x, zero-extended: one PRMT
 __device__ __forceinline__ uint32_t byte_of(uint32_t x, int k) {
   return __byte_perm(x, 0u, 0x4440u | (uint32_t)k);
@@ -151,8 +181,13 @@ __device__ __forceinline__ void eat_codes(Counter &c, const uint4 (&v)[8], uint3
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const bool big = ((v[i].x | v[i].y | v[i].z | v[i].w) & 0xF8F8F8F8u) != 0;
+#if PP_CAT_V2
+      u[i] = make_uint4(onehot8x4_v2(v[i].x, big), onehot8x4_v2(v[i].y, big),
+                        onehot8x4_v2(v[i].z, big), onehot8x4_v2(v[i].w, big));
+#else
       u[i] = make_uint4(onehot8x4(v[i].x, big), onehot8x4(v[i].y, big),
                         onehot8x4(v[i].z, big), onehot8x4(v[i].w, big));
+#endif
       if (!FULL && !((valid >> i) & 1u)) u[i] = z4;
     }
     c.eat8(u, t);
@@ -204,9 +239,16 @@ __device__ __forceinline__ void eat_codes(Counter &c, const uint4 (&v)[8], uint3
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           const uint32_t c0 = byte_of(w4[q], 2 * k), c1 = byte_of(w4[q], 2 * k + 1);
+#if PP_CAT_V2
+          uint32_t l0, h0, l1, h1;
+          onehot64(c0, l0, h0);
+          onehot64(c1, l1, h1);
+          u[2 * q + k] = ok ? make_uint4(l0, h0, l1, h1) : z4;
+#else
           u[2 * q + k] = ok ? make_uint4(onehot32(c0), onehot32(c0 - 32u), onehot32(c1),
                                          onehot32(c1 - 32u))
                             : z4;
+#endif
         }
       }
       c.eat8(u, t);

@@ -55,6 +55,24 @@ def test_random_codes_vs_oracle_and_materialised_onehot(cuda, oracle, dtype):
     assert [int(x) for x in c.cpu()] == [v + 1 for v in want]
 
 
+def test_every_u8_code_at_every_byte_position(cuda, oracle):
+    """All 256 code values in every byte lane of the 16-byte vectors (the
+    one-hot expansion works on packed bytes: codes >= w, >= 128 and the
+    boundary codes w-1, w, 7, 8, 127, 128, 255 must all be exact), mixed into
+    uniform random codes so that vectors with and without large codes occur."""
+    torch, pp = cuda
+    rng = np.random.default_rng(99)
+    base = np.arange(256, dtype=np.uint8)
+    # 17 shifted copies: code v sits at byte position (v + k) mod 16 for every k
+    ex = np.concatenate([np.roll(base, k) for k in range(17)])
+    small = rng.integers(0, 8, 1 << 16).astype(np.uint8)        # vectors of valid codes only
+    uni = rng.integers(0, 256, (1 << 22) + 9).astype(np.uint8)
+    for host in (ex, np.concatenate([small, ex, uni, small])):
+        codes = torch.from_numpy(host).cuda()
+        for w in (8, 16, 32, 64):
+            assert pp.pospopcnt_categories(codes, w) == oracle.categories(host, w), (w, host.size)
+
+
 def test_u16_column_split_across_launches(cuda):
     """Every code in one bin: each thread's u16 column sits at its 65535 limit
     and the launch is split; the total must still be exact."""
