@@ -517,6 +517,28 @@ def main_gpu(args):
             us = q0.elapsed_time(q1) / reps * 1e3
             c4_sweep[str(words)] = {"us_per_call": round(us, 2),
                                     "GBs": round(nb / us / 1e3, 2)}
+        # the same lengths batched: up to 1M arrays of each length (<= 64 MiB)
+        # at byte offset 3, one pp_count_fixed launch, one counter row each
+        out_b = torch.empty(((1 << 20) * 64,), dtype=torch.int64, device=dev)
+        for words in (1, 3, 17, 255, 512, 8192):
+            seg = 8 * words
+            nseg = min(1 << 20, (nbytes - 8) // seg)
+            fb = lambda: _lib.check(lib.pp_count_fixed(buf.data_ptr() + 3, seg, nseg, 64,
+                                                       out_b.data_ptr(), _lib.PP_SEG_OVERWRITE, sp))
+            for _ in range(3):
+                fb()
+            gpu_busy()
+            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            q0.record(st)
+            for _ in range(10):
+                fb()
+            q1.record(st)
+            torch.cuda.synchronize()
+            us = q0.elapsed_time(q1) / 10 * 1e3
+            c4_sweep[f"{words}_batched"] = {"arrays": nseg, "us_per_launch": round(us, 2),
+                                            "ns_per_array": round(us * 1e3 / nseg, 3),
+                                            "in_plus_out_GBs": round((seg + 512) * nseg / us / 1e3, 1)}
+        del out_b
 
     # the paper's read-only "roofline" kernel over the same bytes
     sink = torch.zeros(1, dtype=torch.int64, device=dev)

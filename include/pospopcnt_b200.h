@@ -55,8 +55,10 @@ extern "C" {
 /* flags for the segmented entry points */
 #define PP_SEG_ACCUMULATE 0  /* out[s*w+j] += count (reference semantics)  */
 #define PP_SEG_OVERWRITE  1  /* out[s*w+j]  = count (fresh counter rows)   */
-/* optional launch-shape hint: lanes per segment (8, 16 or 32) in bits 8-15;
- * 0 = automatic (fixed: from seg_bytes; CSR: 32 = one warp per segment)  */
+/* optional launch-shape hint: lanes per segment (1, 8, 16 or 32) in bits 8-15;
+ * 0 = automatic (fixed: 1 up to 1024-byte segments, else from seg_bytes;
+ * CSR: 32 = one warp per segment).  1 = one lane per segment (SWAR counts,
+ * for arrays of a few words; a long segment then runs on a single lane). */
 #define PP_SEG_LANES(g)   ((g) << 8)
 
 PP_API int         pp_abi_version(void);

@@ -243,9 +243,14 @@ int pp_count_categories(const void *codes, size_t ncodes, int code_bytes, int wi
 // Lanes per segment: explicit hint in flags bits 8-15, else from the
 // (average) segment size: one warp per segment from 16 KiB up, 8 lanes
 // (4 segments per warp, 4x fewer transposes per segment) below 8 KiB.
+// Lanes per segment: the hint (1, 8, 16 or 32), else from the segment length:
+// one lane each for tiny fixed segments (SWAR kernel), else G-lane groups.
+static constexpr unsigned long long kLaneAutoMaxBytes = 1024;  // crossover: scripts/seg_small.py
+
 static int seg_lanes(int flags, unsigned long long avg_bytes) {
   const int hint = (flags >> 8) & 0xFF;
-  if (hint == 8 || hint == 16 || hint == 32) return hint;
+  if (hint == 1 || hint == 8 || hint == 16 || hint == 32) return hint;
+  if (avg_bytes <= kLaneAutoMaxBytes) return 1;
   if (avg_bytes >= 16384) return 32;
   if (avg_bytes >= 8192) return 16;
   return 8;

@@ -581,6 +581,141 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
   }
 }
 
+// ---- one lane per segment (tiny arrays) ------------------------------------
+// For arrays of a few words the G-lane kernels spend most of their time in
+// the per-segment flush (warp transposes).  Here each lane owns one segment
+// and counts it with SWAR adds, no cross-lane work at all: the aligned
+// 16-byte vectors covering [p0, e) are masked to the segment, and for
+// b = 0..3 the bits (x >> b) & 0x11111111 are added into nibble counters
+// (nibble n of nl[b] = frame position 4n + b; nh: 32 + 4n + b).  Nibbles
+// take <= 7 vectors (<= 14 per nibble), then spill into byte counters
+// (bl[c] byte m = frame 8m + c), which take <= 18 nibble spills (<= 252),
+// then spill into per-lane u32 counts in shared memory.  The final counts go
+// to shared memory at their folded index i = (p - rot) & 63, so row j of
+// the output is sum_m fr[j + m*w] (flush_fw, accumulate.py:115-130), and the
+// warp writes its 32 consecutive rows with coalesced stores.
+constexpr int kLaneWarps = 4;
+constexpr int kLaneThreads = kLaneWarps * 32;
+constexpr int kLaneStride = 33;  // fr[pos * 33 + lane]
+
+// 0xFF in bytes [lo, hi) of a u32 holding bytes 4q..4q+3 of a vector
+__device__ __forceinline__ uint32_t byte_range_mask(int q, int lo, int hi) {
+  const int a = min(max(lo - 4 * q, 0), 4), b = min(max(4 * q + 4 - hi, 0), 4);
+  uint32_t m1, m2;
+  asm("shl.b32 %0, %1, %2;" : "=r"(m1) : "r"(0xFFFFFFFFu), "r"(8 * a));  // 32 -> 0
+  asm("shr.b32 %0, %1, %2;" : "=r"(m2) : "r"(0xFFFFFFFFu), "r"(8 * b));
+  return m1 & m2;
+}
+
+template <bool FIXED>
+__global__ void __launch_bounds__(kLaneThreads)
+    pp_seglane_kernel(SegArgs a) {
+  __shared__ uint32_t frs[kLaneWarps][64 * kLaneStride];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t *fr = frs[warp];
+  const uintptr_t base = reinterpret_cast<uintptr_t>(a.base);
+  // the caller's view: vectors entirely inside it are read whole, the
+  // others byte by byte (nothing outside the view is ever read)
+  const uintptr_t view_lo = base + (FIXED ? 0ull : a.seg_off[0]);
+  const uintptr_t view_hi = base + (FIXED ? a.nseg * a.seg_bytes : a.seg_off[a.nseg]);
+  const unsigned long long nw = (unsigned long long)gridDim.x * kLaneWarps;
+  for (unsigned long long s0 = ((unsigned long long)blockIdx.x * kLaneWarps + warp) * 32;
+       s0 < a.nseg; s0 += nw * 32) {
+    const unsigned long long s = s0 + lane;
+    unsigned long long b0 = 0, b1 = 0;
+    if (s < a.nseg) {
+      if (FIXED) {
+        b0 = s * a.seg_bytes;
+        b1 = b0 + a.seg_bytes;
+      } else {
+        b0 = a.seg_off[s];
+        b1 = a.seg_off[s + 1];
+        if (b1 < b0) b1 = b0;
+      }
+    }
+    const uintptr_t p0 = base + b0, e = base + b1;
+    const int rot = 8 * (int)(p0 & 7u);
+    uint32_t nl[4] = {0u, 0u, 0u, 0u}, nh[4] = {0u, 0u, 0u, 0u};
+    uint32_t bl[8], bh[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) bl[c] = bh[c] = 0u;
+    bool spilled = false;
+    uint32_t nvec = 0, nnib = 0;
+    auto nib_to_byte = [&]() {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        bl[b] += nl[b] & 0x0F0F0F0Fu;
+        bl[b + 4] += (nl[b] >> 4) & 0x0F0F0F0Fu;
+        bh[b] += nh[b] & 0x0F0F0F0Fu;
+        bh[b + 4] += (nh[b] >> 4) & 0x0F0F0F0Fu;
+        nl[b] = nh[b] = 0u;
+      }
+    };
+    // counts of frame p = 8m + c (+32) -> fr at the folded index (p - rot) & 63
+    auto byte_to_smem = [&](bool first) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int pl = 8 * m + c;
+          uint32_t *dl = fr + ((pl - rot) & 63) * kLaneStride + lane;
+          uint32_t *dh = fr + ((pl + 32 - rot) & 63) * kLaneStride + lane;
+          const uint32_t vl = (bl[c] >> (8 * m)) & 0xFFu, vh = (bh[c] >> (8 * m)) & 0xFFu;
+          *dl = first ? vl : *dl + vl;
+          *dh = first ? vh : *dh + vh;
+        }
+        bl[c] = bh[c] = 0u;
+      }
+    };
+    for (uintptr_t va = p0 & ~(uintptr_t)15; va < e; va += 16) {
+      uint4 v;
+      if (va >= view_lo && va + 16 <= view_hi) {
+        v = __ldg(reinterpret_cast<const uint4 *>(va));
+        if (va < p0 || va + 16 > e) {  // mask to the segment
+          const int lo = va < p0 ? (int)(p0 - va) : 0;
+          const int hi = va + 16 > e ? (int)(e - va) : 16;
+          v.x &= byte_range_mask(0, lo, hi);
+          v.y &= byte_range_mask(1, lo, hi);
+          v.z &= byte_range_mask(2, lo, hi);
+          v.w &= byte_range_mask(3, lo, hi);
+        }
+      } else {
+        v = load_partial(va, p0, e);
+      }
+      // x, z: frame bits 0-31; y, w: 32-63
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        nl[b] += ((v.x >> b) & 0x11111111u) + ((v.z >> b) & 0x11111111u);
+        nh[b] += ((v.y >> b) & 0x11111111u) + ((v.w >> b) & 0x11111111u);
+      }
+      if (++nvec == 7) {
+        nvec = 0;
+        nib_to_byte();
+        if (++nnib == 18) {
+          nnib = 0;
+          byte_to_smem(!spilled);
+          spilled = true;
+        }
+      }
+    }
+    nib_to_byte();
+    byte_to_smem(!spilled);
+    __syncwarp();
+    // rows s0 .. s0 + nrows - 1 are contiguous in out: coalesced stores
+    const int w = a.width;
+    const uint32_t nrows = (uint32_t)min(32ull, a.nseg - s0);
+    unsigned long long *dst = a.out + s0 * (unsigned long long)w;
+    const int lw = __ffs(w) - 1;
+    for (uint32_t idx = lane; idx < nrows * (uint32_t)w; idx += 32) {
+      const uint32_t r = idx >> lw, j = idx & (uint32_t)(w - 1);
+      unsigned long long val = 0ull;
+      for (int i = (int)j; i < 64; i += w) val += fr[i * kLaneStride + r];
+      dst[idx] = a.overwrite ? val : dst[idx] + val;
+    }
+    __syncwarp();
+  }
+}
+
 // Fixed-size segments (pp_count_fixed) fed by a CTA-wide TMA ring.  A chunk
 // is k whole "items" of S = 32/G consecutive segments (one warp's worth), so
 // no segment straddles a stage.  The 8 consumer warps form two teams of 4;
@@ -869,6 +1004,21 @@ static bool seg_use_tma(const SegArgs &a, const DevInfo &di, unsigned *items_per
 cudaError_t launch_segmented(const SegArgs &a, const DevInfo &di, cudaStream_t st) {
   if (a.nseg == 0) return cudaSuccess;
   const int G = a.lanes_per_segment;
+  if (G == 1) {  // one lane per segment
+    static int lane_blocks = 0;
+    if (!lane_blocks) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lane_blocks, pp_seglane_kernel<true>,
+                                                    kLaneThreads, 0);
+      if (lane_blocks < 1) lane_blocks = 1;
+    }
+    const unsigned long long need = (a.nseg + kLaneThreads - 1) / kLaneThreads;
+    const unsigned g = grid_for(need, (unsigned long long)di.num_sms * lane_blocks);
+    if (a.seg_off)
+      pp_seglane_kernel<false><<<g, kLaneThreads, 0, st>>>(a);
+    else
+      pp_seglane_kernel<true><<<g, kLaneThreads, 0, st>>>(a);
+    return cudaGetLastError();
+  }
   unsigned ipc = 0;
   if (seg_use_tma(a, di, &ipc)) {
     const unsigned long long chunks =

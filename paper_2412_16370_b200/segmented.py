@@ -15,6 +15,10 @@ import numpy as np
 from . import _lib
 from .core import InputLengthError, InputView, check_width, is_torch_tensor
 
+# arrays up to this many bytes are counted one lane each (pp_seglane_kernel);
+# the C ABI applies the same bound to fixed-size segments
+LANE_MAX_BYTES = 1024
+
 
 def _device_view(data):
     view = InputView.of(data)
@@ -47,9 +51,10 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
     sequence / numpy array, or a CUDA int64 tensor).  ``out``: CUDA
     (nseg, width) int64 tensor accumulated into (or overwritten when
     ``accumulate=False``); allocated zeroed when None.  Returns ``out``.
-    Asynchronous on the current stream.  ``lanes`` (8, 16 or 32) forces the
-    lanes-per-segment launch shape; by default it follows the mean segment
-    length when the offsets are on the host.
+    Asynchronous on the current stream.  ``lanes`` (1, 8, 16 or 32) forces
+    the lanes-per-segment launch shape; by default it follows the segment
+    lengths when the offsets are on the host (1 when every segment is at most
+    LANE_MAX_BYTES).
     """
     import torch
     check_width(width)
@@ -77,8 +82,12 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
                 raise InputLengthError(f"a segment is not a multiple of the {step}-byte word size")
         offs = torch.as_tensor(offs_np, device=dev)
         if lanes is None and offs_np.size > 1:
+            d = np.diff(offs_np)
             mean = (int(offs_np[-1]) - int(offs_np[0])) // (offs_np.size - 1)
-            lanes = 32 if mean >= 16384 else 16 if mean >= 8192 else 8
+            # one lane per array when every array is tiny (no long outlier
+            # can stall a lane), else G lanes by the mean length
+            lanes = (1 if int(d.max()) <= LANE_MAX_BYTES else
+                     32 if mean >= 16384 else 16 if mean >= 8192 else 8)
     nseg = offs.numel() - 1
     out, fresh = _out_tensor(out, max(nseg, 0), width, dev)
     if nseg <= 0:
@@ -99,8 +108,8 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
 def _lanes_flag(lanes):
     if lanes is None:
         return 0
-    if lanes not in (8, 16, 32):
-        raise ValueError("lanes must be 8, 16 or 32")
+    if lanes not in (1, 8, 16, 32):
+        raise ValueError("lanes must be 1, 8, 16 or 32")
     return lanes << 8
 
 

@@ -50,7 +50,7 @@ def test_c1_exhaustive_sweep_via_segments(cuda, oracle):
         buf = torch.from_numpy(host).cuda()
         doffs = torch.from_numpy(offs).cuda()
         got = None
-        for lanes, path in ((32, 0), (16, 0), (8, 0)):
+        for lanes, path in ((32, 0), (16, 0), (8, 0), (1, 0)):
             # every launch shape must agree
             out = torch.zeros((3 * len(cases), w), dtype=torch.int64, device="cuda")
             rc = lib.pp_count_segmented(buf.data_ptr(), doffs.data_ptr(), 3 * len(cases), w,
@@ -74,7 +74,7 @@ def test_c1_exhaustive_sweep_via_segments(cuda, oracle):
                 dig["sha256_u64_rows"], w
 
 
-@pytest.mark.parametrize("lanes", (None, 8, 16, 32))
+@pytest.mark.parametrize("lanes", (None, 1, 8, 16, 32))
 def test_ragged_random_segments_poison(cuda, oracle, rng, lanes):
     torch, pp = cuda
     for w in (8, 16, 32, 64):
@@ -97,7 +97,35 @@ def test_ragged_random_segments_poison(cuda, oracle, rng, lanes):
         assert np.array_equal(out.cpu().numpy().view(np.uint64), want), w
 
 
-@pytest.mark.parametrize("lanes", (8, 32))
+def test_tiny_arrays_one_lane_each(cuda, oracle, rng):
+    """Arrays of a few words (C4's short lengths, batched): the automatic
+    shape is one lane per array (pp_seglane_kernel).  Fixed sizes at every
+    byte offset of the batch, and ragged tiny arrays from host offsets."""
+    torch, pp = cuda
+    host = np.frombuffer(rng.randbytes((1 << 21) + 64), np.uint8).copy()
+    buf = torch.from_numpy(host).cuda()
+    for w in (8, 16, 32, 64):
+        step = w // 8
+        for seg in sorted({step, 8, 24, 136, 256}):
+            if seg % step:
+                continue
+            for off in (0, 1, 3, 7):
+                nseg = 4099 if seg > 64 else 20011
+                view = pp.InputView(buf, off, nseg * seg)
+                out = pp.pospopcnt_fixed(view, seg, w)
+                offs = (np.arange(nseg + 1, dtype=np.uint64) * seg + off)
+                want = oracle.segments(host, offs, w)
+                assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (w, seg, off)
+        lens = [rng.randrange(0, 257) // step * step for _ in range(7777)]
+        offs = np.zeros(len(lens) + 1, dtype=np.int64)
+        offs[1:] = np.cumsum(lens)
+        view = pp.InputView(buf, 3, int(offs[-1]))
+        out = pp.pospopcnt_segmented(view, offs, w)
+        want = oracle.segments(host, (offs + 3).astype(np.uint64), w)
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), want), w
+
+
+@pytest.mark.parametrize("lanes", (1, 8, 32))
 def test_config_c4_segmented_batch(cuda, oracle, lanes):
     """262,144 independent 4 KiB arrays of Bernoulli(0.01) bits, w=64."""
     torch, pp = cuda
