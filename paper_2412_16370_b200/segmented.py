@@ -70,6 +70,11 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
                 raise ValueError("offsets must be non-decreasing and inside the view")
             if bool((d % step != 0).any()):
                 raise InputLengthError(f"a segment is not a multiple of the {step}-byte word size")
+            if lanes is None:  # validation already synchronised: pick the shape too
+                dmax, total = int(d.max()), int(offs[-1] - offs[0])
+                mean = total // d.numel()
+                lanes = (1 if dmax <= LANE_MAX_BYTES else
+                         32 if mean >= 16384 else 16 if mean >= 8192 else 8)
     else:
         offs_np = np.asarray(offsets, dtype=np.int64)
         if offs_np.ndim != 1 or offs_np.size < 1:

@@ -123,6 +123,9 @@ def test_tiny_arrays_one_lane_each(cuda, oracle, rng):
         out = pp.pospopcnt_segmented(view, offs, w)
         want = oracle.segments(host, (offs + 3).astype(np.uint64), w)
         assert np.array_equal(out.cpu().numpy().view(np.uint64), want), w
+        # device-side offsets: the shape is chosen during validation
+        out = pp.pospopcnt_segmented(view, torch.from_numpy(offs).cuda(), w)
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), want), w
 
 
 @pytest.mark.parametrize("lanes", (1, 8, 32))
