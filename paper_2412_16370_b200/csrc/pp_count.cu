@@ -17,8 +17,11 @@
 // rotate-and-fold of flush_fw (accumulate.py:115-130).
 //
 // Segmented mode: pp_seg_kernel<G>, G lanes per segment.
+#include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "pp_device.cuh"
 #include "pp_internal.h"
@@ -857,45 +860,71 @@ unsigned long long count_chunk_bytes(LoadPath path) {
   return path == LoadPath::kTma ? kTmaStageBytes : kLdgChunkBytes;
 }
 
+// Per-device launch facts, computed once per device (thread-safe: double-
+// checked under a mutex; the kernel attributes are set with `dev` current).
+static cudaError_t compute_device_info(int dev, DevInfo *out) {
+  DevInfo d{};
+  cudaError_t e;
+  if ((e = cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev))) return e;
+  if ((e = cudaDeviceGetAttribute(&d.cc_major, cudaDevAttrComputeCapabilityMajor, dev))) return e;
+  if ((e = cudaDeviceGetAttribute(&d.cc_minor, cudaDevAttrComputeCapabilityMinor, dev))) return e;
+  if ((e = cudaFuncSetAttribute(pp_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kTmaSmemBytes)))
+    return e;
+  if ((e = cudaFuncSetAttribute(pp_tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kTmaSmemBytes)))
+    return e;
+  for (auto k : {pp_tma_kernel<8, PP_CAT_NCW>, pp_tma_kernel<16, PP_CAT_NCW>,
+                 pp_tma_kernel<32, PP_CAT_NCW>, pp_tma_kernel<64, PP_CAT_NCW>})
+    if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)CatShape::kSmem)))
+      return e;
+  for (auto k : {pp_segtma_kernel<8>, pp_segtma_kernel<16>, pp_segtma_kernel<32>})
+    if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kSegTmaSmem)))
+      return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.seg_blocks_per_sm, pp_seg_kernel<8>,
+                                                         kSegThreads, 0)))
+    return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.ldg_blocks_per_sm,
+                                                         pp_count_ldg_kernel, kLdgThreads, 0)))
+    return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.lane_blocks_per_sm,
+                                                         pp_seglane_kernel<true>, kLaneThreads, 0)))
+    return e;
+  d.seg_blocks_per_sm = std::max(d.seg_blocks_per_sm, 1);
+  d.ldg_blocks_per_sm = std::max(d.ldg_blocks_per_sm, 1);
+  d.lane_blocks_per_sm = std::max(d.lane_blocks_per_sm, 1);
+  {  // SMs left free for concurrent work (e.g. NCCL kernels of a sharded job)
+    const char *r = std::getenv("PP_RESERVE_SMS");
+    const int reserve = r ? std::atoi(r) : 0;
+    d.count_sms = (reserve > 0 && reserve < d.num_sms) ? d.num_sms - reserve : d.num_sms;
+  }
+  d.ready = true;
+  *out = d;
+  return cudaSuccess;
+}
+
 cudaError_t device_info(int dev, DevInfo *out) {
-  static DevInfo cache[64];
-  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  if (!cache[dev].ready) {
-    DevInfo d{};
-    cudaError_t e;
-    if ((e = cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev))) return e;
-    if ((e = cudaDeviceGetAttribute(&d.cc_major, cudaDevAttrComputeCapabilityMajor, dev))) return e;
-    if ((e = cudaDeviceGetAttribute(&d.cc_minor, cudaDevAttrComputeCapabilityMinor, dev))) return e;
-    if ((e = cudaFuncSetAttribute(pp_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kTmaSmemBytes)))
-      return e;
-    if ((e = cudaFuncSetAttribute(pp_tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kTmaSmemBytes)))
-      return e;
-    for (auto k : {pp_tma_kernel<8, PP_CAT_NCW>, pp_tma_kernel<16, PP_CAT_NCW>,
-                   pp_tma_kernel<32, PP_CAT_NCW>, pp_tma_kernel<64, PP_CAT_NCW>})
-      if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)CatShape::kSmem)))
-        return e;
-    for (auto k : {pp_segtma_kernel<8>, pp_segtma_kernel<16>, pp_segtma_kernel<32>})
-      if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)kSegTmaSmem)))
-        return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.seg_blocks_per_sm,
-                                                           pp_seg_kernel<8>, kSegThreads, 0)))
-      return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.ldg_blocks_per_sm,
-                                                           pp_count_ldg_kernel, kLdgThreads, 0)))
-      return e;
-    if (d.seg_blocks_per_sm < 1) d.seg_blocks_per_sm = 1;
-    if (d.ldg_blocks_per_sm < 1) d.ldg_blocks_per_sm = 1;
-    {  // SMs left free for concurrent work (e.g. NCCL kernels of a sharded job)
-      const char *r = std::getenv("PP_RESERVE_SMS");
-      const int reserve = r ? std::atoi(r) : 0;
-      d.count_sms = (reserve > 0 && reserve < d.num_sms) ? d.num_sms - reserve : d.num_sms;
+  constexpr int kMaxDev = 64;
+  static DevInfo cache[kMaxDev];
+  static std::atomic<bool> ready[kMaxDev];
+  static std::mutex m;
+  if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+  if (!ready[dev].load(std::memory_order_acquire)) {
+    std::lock_guard<std::mutex> lk(m);
+    if (!ready[dev].load(std::memory_order_relaxed)) {
+      int cur = -1;
+      cudaError_t e = cudaGetDevice(&cur);
+      if (e != cudaSuccess) return e;
+      if (cur != dev && (e = cudaSetDevice(dev)) != cudaSuccess) return e;
+      DevInfo d;
+      e = compute_device_info(dev, &d);
+      if (cur != dev) cudaSetDevice(cur);
+      if (e != cudaSuccess) return e;
+      cache[dev] = d;
+      ready[dev].store(true, std::memory_order_release);
     }
-    d.ready = true;
-    cache[dev] = d;
   }
   *out = cache[dev];
   return cudaSuccess;
@@ -1005,14 +1034,8 @@ cudaError_t launch_segmented(const SegArgs &a, const DevInfo &di, cudaStream_t s
   if (a.nseg == 0) return cudaSuccess;
   const int G = a.lanes_per_segment;
   if (G == 1) {  // one lane per segment
-    static int lane_blocks = 0;
-    if (!lane_blocks) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lane_blocks, pp_seglane_kernel<true>,
-                                                    kLaneThreads, 0);
-      if (lane_blocks < 1) lane_blocks = 1;
-    }
     const unsigned long long need = (a.nseg + kLaneThreads - 1) / kLaneThreads;
-    const unsigned g = grid_for(need, (unsigned long long)di.num_sms * lane_blocks);
+    const unsigned g = grid_for(need, (unsigned long long)di.num_sms * di.lane_blocks_per_sm);
     if (a.seg_off)
       pp_seglane_kernel<false><<<g, kLaneThreads, 0, st>>>(a);
     else

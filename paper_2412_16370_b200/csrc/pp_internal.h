@@ -44,6 +44,7 @@ struct DevInfo {
   int cc_major, cc_minor;
   int seg_blocks_per_sm;
   int ldg_blocks_per_sm;
+  int lane_blocks_per_sm;
   int count_sms;  // SMs the persistent counting grid uses (num_sms - PP_RESERVE_SMS)
   bool ready;
 };
