@@ -123,12 +123,15 @@ PP_API int pp_count_fixed(const void *base, size_t seg_bytes, size_t nseg, int w
 PP_API int pp_count_multi(const void *data, size_t nbytes, int width,
                           unsigned long long *const *targets, int ntargets, void *stream);
 
-/* CUDA IPC for the targets of pp_count_multi (one process per GPU): export a
- * device allocation as a 64-byte handle, open a peer's handle (peer access
- * is enabled lazily), close it again. */
-#define PP_IPC_HANDLE_BYTES 64
-PP_API int pp_ipc_handle(const void *dev_ptr, void *handle64);
-PP_API int pp_ipc_open(const void *handle64, void **dev_ptr);
+/* CUDA IPC for the targets of pp_count_multi (one process per GPU): export
+ * any device pointer (it may lie inside a larger allocation, e.g. a caching
+ * allocator's block) as a 72-byte handle = the allocation's CUDA IPC handle
+ * + the pointer's offset in it; open a peer's handle (peer access is enabled
+ * lazily; the returned pointer includes the offset); close it again with
+ * the pointer pp_ipc_open returned. */
+#define PP_IPC_HANDLE_BYTES 72
+PP_API int pp_ipc_handle(const void *dev_ptr, void *handle72);
+PP_API int pp_ipc_open(const void *handle72, void **dev_ptr);
 PP_API int pp_ipc_close(void *dev_ptr);
 
 /*

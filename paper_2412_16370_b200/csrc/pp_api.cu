@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -77,6 +78,31 @@ int check_device_ptr(const void *p, const char *what) {
     return fail(PP_EARG, "%s must be device memory", what);
   return PP_OK;
 }
+
+// Base address of the device allocation containing p (driver API
+// cuMemGetAddressRange, reached through the runtime's entry-point query so
+// the library needs no link-time libcuda).
+int alloc_base(const void *p, unsigned long long *base) {
+  using GetRange = int (*)(unsigned long long *, size_t *, unsigned long long);
+  static GetRange fn = [] {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<GetRange>(f);
+  }();
+  if (!fn) return fail(PP_ECUDA, "cuMemGetAddressRange entry point unavailable");
+  size_t size = 0;
+  const int r = fn(base, &size, reinterpret_cast<uintptr_t>(p));
+  if (r != 0) return fail(PP_EARG, "cuMemGetAddressRange failed (CUresult %d)", r);
+  return PP_OK;
+}
+
+// pointers returned by pp_ipc_open -> the mapping base to close
+std::mutex g_ipc_m;
+std::map<void *, void *> g_ipc_base;
 
 int count_device(const void *data, size_t nbytes, int width, unsigned long long *counters,
                  cudaStream_t st, const pp::DevInfo &di, bool raw_frame = false) {
@@ -174,27 +200,48 @@ int pp_count_multi(const void *data, size_t nbytes, int width,
   return PP_OK;
 }
 
-int pp_ipc_handle(const void *dev_ptr, void *handle64) {
-  if (!dev_ptr || !handle64) return fail(PP_EARG, "NULL argument");
-  static_assert(sizeof(cudaIpcMemHandle_t) == PP_IPC_HANDLE_BYTES, "IPC handle size");
+int pp_ipc_handle(const void *dev_ptr, void *handle72) {
+  if (!dev_ptr || !handle72) return fail(PP_EARG, "NULL argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) + 8 == PP_IPC_HANDLE_BYTES, "IPC handle size");
+  int rc;
+  if ((rc = check_device_ptr(dev_ptr, "dev_ptr"))) return rc;
+  // the IPC handle names the whole allocation; the offset travels with it
+  unsigned long long base = 0;
+  if ((rc = alloc_base(dev_ptr, &base))) return rc;
   cudaIpcMemHandle_t h;
-  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void *>(dev_ptr));
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base));
   if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
-  std::memcpy(handle64, &h, sizeof h);
+  const unsigned long long off = reinterpret_cast<uintptr_t>(dev_ptr) - base;
+  std::memcpy(handle72, &h, sizeof h);
+  std::memcpy(static_cast<char *>(handle72) + sizeof h, &off, 8);
   return PP_OK;
 }
 
-int pp_ipc_open(const void *handle64, void **dev_ptr) {
-  if (!handle64 || !dev_ptr) return fail(PP_EARG, "NULL argument");
+int pp_ipc_open(const void *handle72, void **dev_ptr) {
+  if (!handle72 || !dev_ptr) return fail(PP_EARG, "NULL argument");
   cudaIpcMemHandle_t h;
-  std::memcpy(&h, handle64, sizeof h);
-  cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  unsigned long long off = 0;
+  std::memcpy(&h, handle72, sizeof h);
+  std::memcpy(&off, static_cast<const char *>(handle72) + sizeof h, 8);
+  void *base = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
   if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  *dev_ptr = static_cast<char *>(base) + off;
+  std::lock_guard<std::mutex> lk(g_ipc_m);
+  g_ipc_base[*dev_ptr] = base;
   return PP_OK;
 }
 
 int pp_ipc_close(void *dev_ptr) {
-  cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  void *base = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_ipc_m);
+    auto it = g_ipc_base.find(dev_ptr);
+    if (it == g_ipc_base.end()) return fail(PP_EARG, "pointer was not returned by pp_ipc_open");
+    base = it->second;
+    g_ipc_base.erase(it);
+  }
+  cudaError_t e = cudaIpcCloseMemHandle(base);
   if (e != cudaSuccess) return cuda_fail(e, "cudaIpcCloseMemHandle");
   return PP_OK;
 }

@@ -66,6 +66,7 @@ class PeerCounters:
         handle = ctypes.create_string_buffer(_lib.PP_IPC_HANDLE_BYTES)
         with torch.cuda.device(self.device):
             _lib.check(self.lib.pp_ipc_handle(self.local.data_ptr(), handle))
+        self.handle = handle.raw  # IPC handle of the allocation + offset of `local` in it
         handles = [handle.raw]
         if self.world > 1:
             handles = [None] * self.world

@@ -47,7 +47,12 @@ def _worker(rank, world, port, total, lead, width, seed):
     full = buf[lead:lead + total]
     want = O.hs512(full.cpu().numpy(), 0, total, width)
     lo, hi = shard_range(total, world, rank)
+    # a small allocation first, so `local` sits inside a caching-allocator
+    # block (an interior pointer: its IPC handle must carry the offset)
+    pad = torch.empty(4096 + 512 * rank, dtype=torch.uint8, device="cuda")
     peers = PeerCounters(device="cuda:0")
+    assert int.from_bytes(peers.handle[64:72], "little") > 0
+    del pad
     try:
         got = pospopcnt_sharded(full[lo:hi], width, peers=peers)
         assert [int(x) for x in got.cpu()] == want, (rank, width)
