@@ -4,10 +4,13 @@
 Default (N=1): BASELINE.json configs[1] = C2, w=8 over a 1 GiB array of
 Bernoulli(0.5) bits generated in place in HBM.  One step = one pass of the
 hot path (pp_count, one launch of the sm_100a kernel) over the whole array.
-Under torchrun (any N, NCCL) each rank counts its own 1 GiB shard of an
-N GiB array (weak scaling) and each step's counters are allreduced,
-pipelined on a side stream; ``--config c5`` is the fixed 64 GiB array split
-over the N ranks (strong scaling).
+Under torchrun (any N) each rank counts its own 1 GiB shard of an N GiB
+array (weak scaling); by default the counter exchange is fused into the
+counting kernel (``pp_count_multi`` adds every CTA's counts into all ranks'
+IPC-mapped counters, no collective per step); ``--exchange nccl`` instead
+allreduces each step's counters over NCCL, pipelined on a side stream.
+``--config c5`` is the fixed 64 GiB array split over the N ranks (strong
+scaling).
 
 Printed JSON keys beyond the base contract:
   roofline       dominant kernel: algorithmic bytes per launch (n input bytes,
@@ -290,9 +293,10 @@ def main_gpu(args):
     # under torchrun (even with one rank) the NCCL path runs: every step ends
     # with the allreduce of the counters; plain `python bench.py` is N=1 local
     use_dist = "LOCAL_RANK" in os.environ or world > 1
-    if use_dist:
+    if use_dist and (args.exchange == "nccl" or args.config == "c3cat"):
         # leave 8 SMs to NCCL so each step's allreduce runs concurrently with
-        # the next count (the count is HBM-bound: 140 SMs saturate it)
+        # the next count (the count is HBM-bound: 140 SMs saturate it); the
+        # fused exchange has no collective kernels and keeps every SM
         os.environ.setdefault("PP_RESERVE_SMS", "8")
     if use_dist:
         dist.init_process_group("nccl", device_id=dev)
