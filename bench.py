@@ -288,6 +288,9 @@ def main_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PP_BENCH_DEVICE / PP_BENCH_BACKEND: test hooks that run N ranks on one
+    # GPU over gloo (tests/test_gpu_bench_dist.py); never set for a measurement
+    local = int(os.environ.get("PP_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     # under torchrun (even with one rank) the NCCL path runs: every step ends
@@ -299,7 +302,11 @@ def main_gpu(args):
         # fused exchange has no collective kernels and keeps every SM
         os.environ.setdefault("PP_RESERVE_SMS", "8")
     if use_dist:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("PP_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     lib = _lib.load()
     st = torch.cuda.current_stream(dev)
     sp = st.cuda_stream
