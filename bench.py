@@ -302,6 +302,9 @@ def main_gpu(args):
         # fused exchange has no collective kernels and keeps every SM
         os.environ.setdefault("PP_RESERVE_SMS", "8")
     if use_dist:
+        # NCCL's own log lines (e.g. "NCCL version ..." under NCCL_DEBUG) go to
+        # stderr: stdout carries exactly one JSON line
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         backend = os.environ.get("PP_BENCH_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
