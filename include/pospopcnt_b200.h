@@ -83,6 +83,16 @@ PP_API int pp_count(const void *data, size_t nbytes, int width,
              unsigned long long *counters, void *stream);
 
 /*
+ * pp_count_sync — pp_count over DEVICE bytes with the result added into HOST
+ * counters: one call = zero a per-thread device scratch, count, copy the w
+ * counters back, synchronise `stream`.  The reference's list-returning call
+ * shape (kernels.py:315-333: pospopcnt(view, w) -> counters) for data that
+ * already lives in HBM, without a caller-side D2H.
+ */
+PP_API int pp_count_sync(const void *data, size_t nbytes, int width,
+                         unsigned long long *host_counters, void *stream);
+
+/*
  * pp_count_host — the same count over a HOST buffer (pinned or pageable):
  * pipelined host->device copies overlapped with counting, result added into
  * HOST counters.  Synchronous.  Replaces the bytes-like path of pospopcnt()

@@ -32,6 +32,7 @@ SIGNATURES = {
     "pp_device_info": (_int, [_int, _vp, _vp, _vp]),
     "pp_count": (_int, [_vp, _sz, _int, _vp, _vp]),
     "pp_count_host": (_int, [_vp, _sz, _int, _vp]),
+    "pp_count_sync": (_int, [_vp, _sz, _int, _vp, _vp]),
     "pp_count_frame": (_int, [_vp, _sz, _vp, _vp]),
     "pp_count_multi": (_int, [_vp, _sz, _int, _vp, _int, _vp]),
     "pp_ipc_handle": (_int, [_vp, _vp]),

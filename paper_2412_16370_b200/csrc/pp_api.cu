@@ -527,7 +527,91 @@ bool host_is_pinned(const void *p) {
   }
   return at.type == cudaMemoryTypeHost;
 }
+// Per-thread small-call context: device scratch + pinned result counters
+// (pp_count_sync), and for small host inputs a 1 MiB pinned staging buffer,
+// a 1 MiB device buffer and a stream, so a small pp_count_host is one
+// memcpy + five stream operations + one synchronisation.
+constexpr size_t kSmallHost = 1u << 20;
+struct SyncCtx {
+  int dev = -1;
+  unsigned long long *dcnt = nullptr, *hcnt = nullptr;
+  void *pin = nullptr, *dbuf = nullptr;
+  cudaStream_t st = nullptr;
+  cudaError_t ensure(int d) {
+    if (dev == d) return cudaSuccess;
+    // a previous device's buffers are left to process exit (small)
+    dcnt = hcnt = nullptr;
+    pin = dbuf = nullptr;
+    st = nullptr;
+    dev = -1;
+    cudaError_t e;
+    if ((e = cudaMalloc(&dcnt, 64 * sizeof(unsigned long long)))) return e;
+    if ((e = cudaMallocHost(&hcnt, 64 * sizeof(unsigned long long)))) return e;
+    dev = d;
+    return cudaSuccess;
+  }
+  cudaError_t ensure_small_host() {
+    cudaError_t e;
+    if (!pin && (e = cudaMallocHost(&pin, kSmallHost))) return e;
+    if (!dbuf && (e = cudaMalloc(&dbuf, kSmallHost))) return e;
+    if (!st && (e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking))) return e;
+    return cudaSuccess;
+  }
+};
+thread_local SyncCtx g_sync;
+
+// Count nbytes (<= kSmallHost) of host memory through the small-call buffers.
+int count_small_host(const void *host, size_t nbytes, int width, unsigned long long *out,
+                     const pp::DevInfo &di) {
+  SyncCtx &c = g_sync;
+  cudaError_t e;
+  if ((e = c.ensure_small_host())) return cuda_fail(e, "pp_count_host setup");
+  if (nbytes >= (256u << 10))
+    CopyPool::get().copy(c.pin, host, nbytes);
+  else
+    std::memcpy(c.pin, host, nbytes);
+  // same byte alignment on the device as on the host is not needed: counts
+  // of a word-complete range do not depend on its address
+  if ((e = cudaMemcpyAsync(c.dbuf, c.pin, nbytes, cudaMemcpyHostToDevice, c.st)))
+    return cuda_fail(e, "cudaMemcpyAsync");
+  if ((e = cudaMemsetAsync(c.dcnt, 0, (size_t)width * 8, c.st))) return cuda_fail(e, "memset");
+  int rc;
+  if ((rc = count_device(c.dbuf, nbytes, width, c.dcnt, c.st, di))) return rc;
+  if ((e = cudaMemcpyAsync(c.hcnt, c.dcnt, (size_t)width * 8, cudaMemcpyDeviceToHost, c.st)))
+    return cuda_fail(e, "cudaMemcpyAsync");
+  if ((e = cudaStreamSynchronize(c.st))) return cuda_fail(e, "cudaStreamSynchronize");
+  for (int j = 0; j < width; ++j) out[j] += c.hcnt[j];
+  return PP_OK;
+}
 }  // namespace
+
+int pp_count_sync(const void *data, size_t nbytes, int width, unsigned long long *host_counters,
+                  void *stream) {
+  if (!width_ok(width)) return fail(PP_EWIDTH, "word width must be one of (8, 16, 32, 64), got %d", width);
+  if (nbytes % (size_t)(width / 8))
+    return fail(PP_ELENGTH, "%zu bytes is not a multiple of the %d-byte word size", nbytes,
+                width / 8);
+  if (!host_counters) return fail(PP_EARG, "host_counters is NULL");
+  if (nbytes == 0) return PP_OK;
+  int rc;
+  if ((rc = check_device_ptr(data, "data"))) return rc;
+  pp::DevInfo di;
+  if ((rc = current_devinfo(&di))) return rc;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaError_t e = g_sync.ensure(dev);
+  if (e != cudaSuccess) return cuda_fail(e, "pp_count_sync setup");
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if ((e = cudaMemsetAsync(g_sync.dcnt, 0, (size_t)width * 8, st)))
+    return cuda_fail(e, "cudaMemsetAsync");
+  if ((rc = count_device(data, nbytes, width, g_sync.dcnt, st, di))) return rc;
+  if ((e = cudaMemcpyAsync(g_sync.hcnt, g_sync.dcnt, (size_t)width * 8, cudaMemcpyDeviceToHost,
+                           st)))
+    return cuda_fail(e, "cudaMemcpyAsync");
+  if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "cudaStreamSynchronize");
+  for (int j = 0; j < width; ++j) host_counters[j] += g_sync.hcnt[j];
+  return PP_OK;
+}
 
 int pp_count_host(const void *host_data, size_t nbytes, int width,
                   unsigned long long *host_counters) {
@@ -543,11 +627,22 @@ int pp_count_host(const void *host_data, size_t nbytes, int width,
   if ((rc = current_devinfo(&di))) return rc;
   int dev = 0;
   cudaGetDevice(&dev);
-  cudaError_t e = g_host.ensure(dev);
+  cudaError_t e;
+  if (nbytes <= kSmallHost) {
+    if ((e = g_sync.ensure(dev))) return cuda_fail(e, "pp_count_host setup");
+    return count_small_host(host_data, nbytes, width, host_counters, di);
+  }
+  e = g_host.ensure(dev);
   if (e != cudaSuccess) return cuda_fail(e, "pp_count_host setup");
   HostCtx &h = g_host;
-  // below ~32 MiB the driver's own pageable staging is as fast
-  const bool staged = !host_is_pinned(host_data) && nbytes >= (32u << 20);
+  // pageable sources of >= 32 MiB go through our pinned ring + parallel copy
+  // pool; below that the driver's own pageable path is as fast (both are
+  // host-memcpy-bound at 7-26 GB/s for 1-32 MiB: scripts/host_path_ab.py)
+  static const size_t stage_min = [] {  // PP_HOST_STAGE_MIN: A/B of the threshold
+    const char *env = std::getenv("PP_HOST_STAGE_MIN");
+    return env ? (size_t)std::strtoull(env, nullptr, 10) : (size_t)(32u << 20);
+  }();
+  const bool staged = nbytes >= stage_min && !host_is_pinned(host_data);
   // staged chunks are smaller so the pool copy of chunk i+1 overlaps the DMA
   // of chunk i even for inputs of a few chunks
   static const size_t stage_chunk = [] {
@@ -556,7 +651,11 @@ int pp_count_host(const void *host_data, size_t nbytes, int width,
     c &= ~(size_t)63;
     return (c < (1u << 20) || c > kChunk) ? (size_t)(8u << 20) : c;
   }();
-  const size_t chunk = staged ? stage_chunk : kChunk;
+  // a few chunks even for mid-size inputs, so the pool copy of chunk i + 1
+  // overlaps the DMA of chunk i
+  const size_t chunk =
+      !staged ? kChunk
+              : std::min(stage_chunk, std::max<size_t>(kSmallHost, (nbytes / 4 + 63) & ~(size_t)63));
   if (staged && (e = h.ensure_pinned())) return cuda_fail(e, "pp_count_host staging");
   if ((e = cudaMemsetAsync(h.dcnt, 0, 64 * sizeof(unsigned long long), h.count)))
     return cuda_fail(e, "cudaMemsetAsync");

@@ -88,6 +88,14 @@ def _device_scratch(device):
     return t
 
 
+def _host_result():
+    """Per-thread u64[64] host buffer the C calls write results into."""
+    r = getattr(_tls, "result", None)
+    if r is None:
+        r = _tls.result = np.zeros(W_MAX, dtype=np.uint64)
+    return r
+
+
 def _device_counters(counters, w, device):
     """counters usable in place on `device`, or None."""
     if is_torch_tensor(counters) and counters.is_cuda:
@@ -160,23 +168,32 @@ class B200Kernel:
         if not base.is_contiguous():
             raise ValueError("input tensor must be contiguous")
         dev = base.device
-        with torch.cuda.device(dev):
+        # switch devices only when needed (the context manager costs ~us per call)
+        switch = dev.index != torch.cuda.current_device()
+        if switch:
+            prev = torch.cuda.current_device()
+            torch.cuda.set_device(dev)
+        try:
             stream = torch.cuda.current_stream(dev).cuda_stream
             ptr = base.data_ptr() + view.offset
             dc = _device_counters(counters, w, dev)
             if dc is not None:
                 _lib.check(lib.pp_count(ptr, view.nbytes, w, dc.data_ptr(), stream))
                 return counters
-            scratch = _device_scratch(dev)
-            scratch.zero_()
-            _lib.check(lib.pp_count(ptr, view.nbytes, w, scratch.data_ptr(), stream))
-            vals = scratch[:w].cpu().numpy().view(np.uint64)
+            # host-side counters: count, copy back and synchronise in one C call
+            vals = _host_result()
+            vals[:w] = 0
+            _lib.check(lib.pp_count_sync(ptr, view.nbytes, w, vals.ctypes.data, stream))
+        finally:
+            if switch:
+                torch.cuda.set_device(prev)
         _add_into(counters, vals, w)
         return counters
 
     def _run_host(self, lib, view, w, counters):
         ptr, keep = _host_u8(view.base, view.offset, view.nbytes)
-        out = np.zeros(W_MAX, dtype=np.uint64)
+        out = _host_result()
+        out[:] = 0
         dev_idx = None
         if is_torch_tensor(counters) and counters.is_cuda:
             dev_idx = counters.device.index
