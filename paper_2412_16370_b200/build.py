@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpospopcnt_b200.so")
-SOURCES = ("pp_api.cu", "pp_count.cu", "pp_categories.cu", "pp_gen.cu")
+SOURCES = ("pp_api.cu", "pp_count.cu", "pp_segmented.cu", "pp_categories.cu", "pp_gen.cu")
 HEADERS = ("pp_device.cuh", "pp_internal.h")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -50,6 +50,13 @@ struct DevInfo {
 };
 
 cudaError_t device_info(int dev, DevInfo *out);
+// segmented kernels' attributes and occupancy into *d (pp_segmented.cu)
+cudaError_t segmented_setup(DevInfo *d);
+
+inline unsigned grid_for(unsigned long long nchunks, unsigned long long cap) {
+  const unsigned long long g = nchunks < cap ? nchunks : cap;
+  return (unsigned)(g ? g : 1);
+}
 
 // Fills head/body/tail fields of a (given data pointer, nbytes, chunk size).
 void split_range(const uint8_t *data, unsigned long long nbytes,
