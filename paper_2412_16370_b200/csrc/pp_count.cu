@@ -23,6 +23,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 
 #include "pp_device.cuh"
@@ -30,7 +31,12 @@
 
 namespace pp {
 
+#ifndef PP_TIMELINE
+#define PP_TIMELINE 0
+#endif
 constexpr int kTmaConsumerWarps = 8;
+constexpr unsigned long long kNoChunk = ~0ull;
+constexpr int kSchedSlotsAlloc = 256;  // = kSchedSlots (scheduler slots per device)
 constexpr int kTmaStages = 3;  // 3 x 32 KiB: best of the scripts/bw_probe.cu sweep (profiles/)
 constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
 constexpr int kTmaStageVecs = kTmaConsumerWarps * 32 * 8;  // 2048 x 16 B = 32 KiB
@@ -270,6 +276,26 @@ __device__ __forceinline__ void count_code_edges(Counter &c, const uint8_t *head
   c.co += wcount(ok ? onehot32(code - 32u) : 0u, t);
 }
 
+// PP_TIMELINE (diagnostic builds only, scripts/timeline.py): %globaltimer
+// stamps per CTA of the counting kernel -- entry, first copy issued, first
+// stage consumed, last copy issued, last chunk consumed, epilogue start, end.
+#if PP_TIMELINE
+__device__ unsigned long long pp_tl[1024][8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PP_TL(k)                                                   \
+  do {                                                             \
+    if (MODE == 1 && blockIdx.x < 1024) pp_tl[blockIdx.x][k] = gtime(); \
+  } while (0)
+#else
+#define PP_TL(k) \
+  do {           \
+  } while (0)
+#endif
+
 // MODE 0: read-only roofline (XOR of every word), MODE 1: positional count,
 // MODE 8/16/32/64: fused one-hot producer over u8 codes at that width.
 template <int MODE, int NCW = kTmaConsumerWarps>
@@ -282,9 +308,11 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + kTmaStages * Sh::kStageBytes);
   uint64_t *empty = full + kTmaStages;
   __shared__ unsigned long long frame[64];
+  __shared__ unsigned long long chunk_id[kTmaStages];  // written before the stage's arrival
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
+    PP_TL(0);
     for (int s = 0; s < kTmaStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NCW);
@@ -303,19 +331,32 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       // previous grid's tail; its outputs (possibly our input) are complete
       // and visible only after this wait
       asm volatile("griddepcontrol.wait;" ::: "memory");
+      PP_TL(1);
       uint32_t stage = 0, phase = 0;
-      for (unsigned long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+      // chunk sequence: chunk blockIdx.x first, then either dynamic (ticket
+      // t of a shared counter = chunk gridDim.x + t, so every CTA finishes
+      // within about one chunk of the others) or the static grid stride
+      unsigned long long ch = blockIdx.x;
+      for (;;) {
         mbar_wait(&empty[stage], phase ^ 1);
+        if (ch >= nchunks) {  // tell the consumers to stop: no bytes, one arrival
+          chunk_id[stage] = kNoChunk;
+          mbar_arrive(&full[stage]);
+          break;
+        }
+        chunk_id[stage] = ch;
         const unsigned long long off = ch * Sh::kStageBytes;
         const unsigned long long rem = a.body_bytes - off;
         const uint32_t bytes = (uint32_t)(rem < Sh::kStageBytes ? rem : Sh::kStageBytes);
         mbar_arrive_expect_tx(&full[stage], bytes);
         bulk_g2s(stages + stage * Sh::kStageVecs, a.body + off, bytes, &full[stage], pol);
+        ch = a.sched ? gridDim.x + (unsigned long long)atomicAdd(a.sched, 1u) : ch + gridDim.x;
         if (++stage == kTmaStages) {
           stage = 0;
           phase ^= 1;
         }
       }
+      PP_TL(3);
       // every load of this CTA is in flight: the next launch on the stream
       // (programmatic dependent launch) may start filling its own ring
       asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -328,8 +369,11 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     uint32_t xs = 0;  // read-only roofline accumulator
     uint32_t stage = 0, phase = 0;
     const uint32_t tid = threadIdx.x;
-    for (unsigned long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    for (bool first = true;; first = false) {
       mbar_wait(&full[stage], phase);
+      const unsigned long long ch = chunk_id[stage];
+      if (ch == kNoChunk) break;
+      if (first && threadIdx.x == 0) PP_TL(2);
       const uint4 *sv = stages + stage * Sh::kStageVecs;
       uint4 v[8];
       uint32_t valid = 0xFFu;  // vectors present in this (possibly partial) chunk
@@ -367,6 +411,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       }
     }
     if (kCount) {
+      if (threadIdx.x == 0) PP_TL(4);
       c.finish(t);
       if (blockIdx.x == 0 && warp == 0) {
         if (MODE == 1)
@@ -385,7 +430,18 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) PP_TL(5);
   if (kCount) fold_frame_to_counters(frame, a);
+  if (threadIdx.x == 0) PP_TL(6);
+  if (a.sched && threadIdx.x == 0) {
+    // every producer of the grid has drawn its last ticket before its CTA
+    // got here: the last CTA re-arms the scheduler slot for the next launch
+    // on this stream (stream order, or griddepcontrol.wait under PDL)
+    if (atomicAdd(a.sched + 1, 1u) == gridDim.x - 1) {
+      atomicExch(a.sched, 0u);
+      atomicExch(a.sched + 1, 0u);
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kLdgThreads)
@@ -474,6 +530,11 @@ static cudaError_t compute_device_info(int dev, DevInfo *out) {
     const int reserve = r ? std::atoi(r) : 0;
     d.count_sms = (reserve > 0 && reserve < d.num_sms) ? d.num_sms - reserve : d.num_sms;
   }
+  {  // dynamic scheduler slots (sched_slot), zeroed once
+    const size_t bytes = 2 * kSchedSlotsAlloc * sizeof(unsigned int);
+    if ((e = cudaMalloc(&d.sched, bytes))) return e;
+    if ((e = cudaMemset(d.sched, 0, bytes))) return e;
+  }
   d.ready = true;
   *out = d;
   return cudaSuccess;
@@ -518,12 +579,48 @@ static unsigned long long pdl_max_body() {  // PP_PDL_MAX_MIB overrides (A/B run
   return v;
 }
 
+// Dynamic chunk scheduling: every stream gets its own scheduler slot (keyed
+// by the stream's unique id, so a recycled handle cannot alias a live
+// stream); launches on one stream are ordered, so a slot is never shared by
+// two running grids.  Captured launches (a graph may be replayed on several
+// streams at once) and streams beyond kSchedSlots use the static order.
+// PP_STATIC_SCHED=1 forces the static order (A/B runs).
+constexpr int kSchedSlots = kSchedSlotsAlloc;
+constexpr unsigned long long kDynMinChunks = 4096;  // 128 MiB of 32 KiB chunks
+static unsigned int *sched_slot(const DevInfo &di, cudaStream_t st) {
+  static const bool off = std::getenv("PP_STATIC_SCHED") != nullptr;
+  if (off || !di.sched) return nullptr;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  unsigned long long id = 0;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone ||
+      cudaStreamGetId(st, &id) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  static std::mutex m;
+  static std::map<std::pair<unsigned int *, unsigned long long>, int> slots;
+  static std::map<unsigned int *, int> used;
+  std::lock_guard<std::mutex> lk(m);
+  const auto key = std::make_pair(di.sched, id);
+  const auto it = slots.find(key);
+  if (it != slots.end()) return di.sched + 2 * it->second;
+  int &n = used[di.sched];
+  if (n >= kSchedSlots) return nullptr;
+  slots[key] = n;
+  return di.sched + 2 * (n++);
+}
+
 template <typename Kern>
 static cudaError_t launch_tma(Kern kernel, unsigned grid, unsigned block, size_t smem,
-                              cudaStream_t st, const CountArgs &a, unsigned long long *sink,
-                              bool want_pdl) {
+                              cudaStream_t st, const CountArgs &a0, unsigned long long *sink,
+                              bool want_pdl, const DevInfo &di) {
   static const bool pdl_off = std::getenv("PP_NO_PDL") != nullptr;
   const bool pdl = want_pdl && !pdl_off;
+  CountArgs a = a0;
+  // the dynamic order pays off once a CTA streams tens of chunks (+6 % at
+  // 256 MiB, +2 % at 1 GiB); below that the static order has no tail to
+  // even out and saves the slot lookup (scripts/pdl_sweep.py)
+  a.sched = a.nchunks >= kDynMinChunks ? sched_slot(di, st) : nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
@@ -542,7 +639,7 @@ cudaError_t launch_count(const CountArgs &a, LoadPath path, const DevInfo &di,
   if (path == LoadPath::kTma) {
     const unsigned g = grid_for(a.nchunks, (unsigned long long)di.count_sms);
     cudaError_t e = launch_tma(pp_tma_kernel<1>, g, kTmaThreads, kTmaSmemBytes, st, a, nullptr,
-                               a.body_bytes < pdl_max_body());
+                               a.body_bytes < pdl_max_body(), di);
     if (e != cudaSuccess) return e;
   } else {
     const unsigned g =
@@ -557,16 +654,16 @@ cudaError_t launch_count_codes8(const CountArgs &a, const DevInfo &di, cudaStrea
   switch (a.width) {
     case 8:
       return launch_tma(pp_tma_kernel<8, PP_CAT_NCW>, g, CatShape::kThreads, CatShape::kSmem, st,
-                        a, nullptr, true);
+                        a, nullptr, true, di);
     case 16:
       return launch_tma(pp_tma_kernel<16, PP_CAT_NCW>, g, CatShape::kThreads, CatShape::kSmem,
-                        st, a, nullptr, true);
+                        st, a, nullptr, true, di);
     case 32:
       return launch_tma(pp_tma_kernel<32, PP_CAT_NCW>, g, CatShape::kThreads, CatShape::kSmem,
-                        st, a, nullptr, true);
+                        st, a, nullptr, true, di);
     default:
       return launch_tma(pp_tma_kernel<64, PP_CAT_NCW>, g, CatShape::kThreads, CatShape::kSmem,
-                        st, a, nullptr, true);
+                        st, a, nullptr, true, di);
   }
   return cudaGetLastError();
 }
@@ -575,7 +672,13 @@ cudaError_t launch_readonly(const CountArgs &a, unsigned long long *sink, const 
                             cudaStream_t st) {
   const unsigned g = grid_for(a.nchunks, (unsigned long long)di.count_sms);
   return launch_tma(pp_tma_kernel<0>, g, kTmaThreads, kTmaSmemBytes, st, a, sink,
-                    a.body_bytes < pdl_max_body());
+                    a.body_bytes < pdl_max_body(), di);
 }
 
 }  // namespace pp
+
+#if PP_TIMELINE
+extern "C" __attribute__((visibility("default"))) int pp_debug_timeline(unsigned long long *out) {
+  return (int)cudaMemcpyFromSymbol(out, pp::pp_tl, sizeof(pp::pp_tl));
+}
+#endif

@@ -24,6 +24,9 @@ struct CountArgs {
   // that receive the same counts as `counters`
   int nextra;
   unsigned long long *extra[15];
+  // dynamic chunk scheduler slot {next ticket, CTAs done} (per stream), or
+  // nullptr for the static grid-stride order (graph capture, slots exhausted)
+  unsigned int *sched;
 };
 
 struct SegArgs {
@@ -46,6 +49,7 @@ struct DevInfo {
   int ldg_blocks_per_sm;
   int lane_blocks_per_sm;
   int count_sms;  // SMs the persistent counting grid uses (num_sms - PP_RESERVE_SMS)
+  unsigned int *sched;  // kSchedSlots x {next, done}, zeroed (device memory)
   bool ready;
 };
 
