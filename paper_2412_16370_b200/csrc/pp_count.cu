@@ -566,15 +566,17 @@ cudaError_t device_info(int dev, DevInfo *out) {
 }
 
 // Launch a TMA-ring kernel, with programmatic dependent launch when `pdl`:
-// two CTAs of consecutive launches fit on one SM, so launch i+1 streams while
-// launch i drains its tail.  Measured (scripts/pdl_sweep.py): 4.9 -> 3.8 us
-// per 1 MiB call, 14.4 -> 10.8 us per 64 MiB, +7 % at 256 MiB, but -1 % at
-// 1 GiB where the overlapping CTAs contend; hence the size cut below.
-// PP_NO_PDL=1 disables it (A/B runs).
-static unsigned long long pdl_max_body() {  // PP_PDL_MAX_MIB overrides (A/B runs)
+// launch i+1's CTAs start, set up their rings and park in
+// griddepcontrol.wait while launch i drains its tail, hiding the launch gap.
+// Measured (scripts/pdl_sweep.py, profiles/r1_pdl_sweep.md): 4.9 -> 3.2 us
+// per 4 MiB call, 14.4 -> 13.4 us per 64 MiB; at 1 GiB it cost 1-2 % with
+// the static chunk order (CTAs finishing up to 8 us apart) and gains 1 % with
+// the dynamic order (148.0 -> 146.4 us), so it is on at every size.
+// PP_NO_PDL=1 disables it, PP_PDL_MAX_MIB caps it (A/B runs).
+static unsigned long long pdl_max_body() {
   static const unsigned long long v = [] {
     const char *e = std::getenv("PP_PDL_MAX_MIB");
-    return (e ? std::strtoull(e, nullptr, 10) : 512ull) << 20;
+    return e ? std::strtoull(e, nullptr, 10) << 20 : ~0ull;
   }();
   return v;
 }
