@@ -35,7 +35,6 @@ namespace pp {
 #define PP_TIMELINE 0
 #endif
 constexpr int kTmaConsumerWarps = 8;
-constexpr unsigned long long kNoChunk = ~0ull;
 constexpr int kSchedSlotsAlloc = 256;  // = kSchedSlots (scheduler slots per device)
 constexpr int kTmaStages = 3;  // 3 x 32 KiB: best of the scripts/bw_probe.cu sweep (profiles/)
 constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
@@ -589,7 +588,7 @@ static unsigned long long pdl_max_body() {
 // PP_STATIC_SCHED=1 forces the static order (A/B runs).
 constexpr int kSchedSlots = kSchedSlotsAlloc;
 constexpr unsigned long long kDynMinChunks = 4096;  // 128 MiB of 32 KiB chunks
-static unsigned int *sched_slot(const DevInfo &di, cudaStream_t st) {
+unsigned int *sched_slot(const DevInfo &di, cudaStream_t st) {
   static const bool off = std::getenv("PP_STATIC_SCHED") != nullptr;
   if (off || !di.sched) return nullptr;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;

@@ -37,7 +37,8 @@ struct SegArgs {
   unsigned long long *out;
   int width;
   int overwrite;
-  int lanes_per_segment;  // G in {8, 16, 32}
+  int lanes_per_segment;  // G in {1, 8, 16, 32}
+  unsigned int *sched;    // dynamic chunk scheduler slot (TMA ring kernel), or nullptr
 };
 
 enum class LoadPath : int { kTma = 0, kLdg = 1 };
@@ -56,6 +57,12 @@ struct DevInfo {
 cudaError_t device_info(int dev, DevInfo *out);
 // segmented kernels' attributes and occupancy into *d (pp_segmented.cu)
 cudaError_t segmented_setup(DevInfo *d);
+
+// "no chunk": the TMA producers' stop sentinel in a stage's chunk-id slot
+constexpr unsigned long long kNoChunk = ~0ull;
+// Per-stream dynamic scheduler slot {next ticket, CTAs done} on di's device,
+// or nullptr (graph capture, slots exhausted, PP_STATIC_SCHED).
+unsigned int *sched_slot(const DevInfo &di, cudaStream_t st);
 
 inline unsigned grid_for(unsigned long long nchunks, unsigned long long cap) {
   const unsigned long long g = nchunks < cap ? nchunks : cap;

@@ -348,6 +348,7 @@ __global__ void __launch_bounds__(kSegTmaThreads, 1)
   uint4 *stages = reinterpret_cast<uint4 *>(smem);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + kSegTmaStages * kSegTmaStageBytes);
   uint64_t *empty = full + kSegTmaStages;
+  __shared__ unsigned long long chunk_id[kSegTmaStages];  // written before the stage's arrival
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kSegTmaStages; ++s) {
@@ -368,29 +369,39 @@ __global__ void __launch_bounds__(kSegTmaThreads, 1)
   if (warp == kSegTmaWarps) {
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      uint32_t j = 0;
-      for (unsigned long long ch = blockIdx.x; ch < nchunks; ch += gridDim.x, ++j) {
+      // chunk blockIdx.x first, then tickets of the stream's scheduler slot
+      // (chunk gridDim.x + ticket) or the static grid stride; one stop
+      // sentinel per team once the chunks are gone
+      unsigned long long ch = blockIdx.x;
+      int stops = 0;
+      for (uint32_t j = 0;; ++j) {
         const uint32_t stage = j % kSegTmaStages;
         mbar_wait(&empty[stage], ((j / kSegTmaStages) & 1u) ^ 1u);
+        if (ch >= nchunks) {
+          chunk_id[stage] = kNoChunk;
+          mbar_arrive(&full[stage]);
+          if (++stops == kSegTmaTeams) break;
+          continue;
+        }
+        chunk_id[stage] = ch;
         const unsigned long long off = ch * chunk_bytes;
         const unsigned long long rem = total - off;
         const uint32_t bytes = (uint32_t)(rem < chunk_bytes ? rem : chunk_bytes);
         mbar_arrive_expect_tx(&full[stage], bytes);
         bulk_g2s(stages + stage * kStageVecs, a.base + off, bytes, &full[stage], pol);
+        ch = a.sched ? gridDim.x + (unsigned long long)atomicAdd(a.sched, 1u) : ch + gridDim.x;
       }
     }
-    return;
-  }
-
+  } else {
   const uint32_t team = warp / kSegTmaTeamWarps, wi = warp % kSegTmaTeamWarps;
   const uint32_t r = lane % G, sl = lane / G;
   const uint32_t segv = (uint32_t)(seg_bytes >> 4);  // vectors per segment
   const TC t = make_tc(lane);
-  uint32_t j = team;
-  for (unsigned long long ch = blockIdx.x + (unsigned long long)team * gridDim.x; ch < nchunks;
-       ch += (unsigned long long)kSegTmaTeams * gridDim.x, j += kSegTmaTeams) {
+  for (uint32_t j = team;; j += kSegTmaTeams) {
     const uint32_t stage = j % kSegTmaStages;
     mbar_wait(&full[stage], (j / kSegTmaStages) & 1u);
+    const unsigned long long ch = chunk_id[stage];
+    if (ch == kNoChunk) break;
     const uint4 *sv = stages + stage * kStageVecs;
     const unsigned long long seg0 = ch * segs_per_chunk;
     bool released = false;
@@ -428,6 +439,14 @@ __global__ void __launch_bounds__(kSegTmaThreads, 1)
     if (!released) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
+    }
+  }
+  }
+  __syncthreads();
+  if (a.sched && threadIdx.x == 0) {  // the last CTA re-arms the scheduler slot
+    if (atomicAdd(a.sched + 1, 1u) == gridDim.x - 1) {
+      atomicExch(a.sched, 0u);
+      atomicExch(a.sched + 1, 0u);
     }
   }
 }
@@ -487,12 +506,14 @@ cudaError_t launch_segmented(const SegArgs &a, const DevInfo &di, cudaStream_t s
     const unsigned long long chunks =
         (a.nseg + (unsigned long long)ipc * (32 / G) - 1) / ((unsigned long long)ipc * (32 / G));
     const unsigned g = grid_for(chunks, (unsigned long long)di.num_sms);
+    SegArgs b = a;  // dynamic chunk order once CTAs stream tens of chunks
+    b.sched = chunks >= 16ull * g ? sched_slot(di, st) : nullptr;
     if (G == 8)
-      pp_segtma_kernel<8><<<g, kSegTmaThreads, kSegTmaSmem, st>>>(a, ipc);
+      pp_segtma_kernel<8><<<g, kSegTmaThreads, kSegTmaSmem, st>>>(b, ipc);
     else if (G == 16)
-      pp_segtma_kernel<16><<<g, kSegTmaThreads, kSegTmaSmem, st>>>(a, ipc);
+      pp_segtma_kernel<16><<<g, kSegTmaThreads, kSegTmaSmem, st>>>(b, ipc);
     else
-      pp_segtma_kernel<32><<<g, kSegTmaThreads, kSegTmaSmem, st>>>(a, ipc);
+      pp_segtma_kernel<32><<<g, kSegTmaThreads, kSegTmaSmem, st>>>(b, ipc);
     return cudaGetLastError();
   }
   const unsigned long long segs_per_block = (kSegThreads / 32) * (32 / G);
