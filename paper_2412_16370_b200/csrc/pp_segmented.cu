@@ -137,7 +137,10 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
   const unsigned long long gw = (blockIdx.x * (unsigned long long)kSegThreads + threadIdx.x) >> 5;
   const unsigned long long nw = (gridDim.x * (unsigned long long)kSegThreads) >> 5;
   const TC t = make_tc(lane);
-  for (unsigned long long first = gw * S; first < a.nseg; first += nw * S) {
+  // group gw first, then (a.sched) tickets of the stream's scheduler slot,
+  // one per group of S segments (group nw + ticket), else the grid stride:
+  // ragged lengths no longer leave a few warps with most of the bytes
+  for (unsigned long long first = gw * S; first < a.nseg;) {
     const unsigned long long s = first + sl;
     const SegGeom g = seg_geom(a, s);
     GroupCounter<G, PP_SEG_SMEM_COUNTS> c;
@@ -175,6 +178,20 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
     }
     c.finish(t);
     if (s < a.nseg) write_row(a, s, g.p0, c, lane);
+    if (a.sched) {
+      unsigned long long tk = 0;
+      if (lane == 0) tk = atomicAdd(a.sched, 1u);
+      first = (nw + __shfl_sync(FULL, tk, 0)) * S;
+    } else {
+      first += nw * S;
+    }
+  }
+  if (a.sched) {  // the last CTA re-arms the scheduler slot
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(a.sched + 1, 1u) == gridDim.x - 1) {
+      atomicExch(a.sched, 0u);
+      atomicExch(a.sched + 1, 0u);
+    }
   }
 }
 
@@ -519,12 +536,14 @@ cudaError_t launch_segmented(const SegArgs &a, const DevInfo &di, cudaStream_t s
   const unsigned long long segs_per_block = (kSegThreads / 32) * (32 / G);
   const unsigned long long need = (a.nseg + segs_per_block - 1) / segs_per_block;
   const unsigned g = grid_for(need, (unsigned long long)di.num_sms * di.seg_blocks_per_sm);
+  SegArgs b = a;  // dynamic group order once warps see several groups each
+  b.sched = need >= 4ull * g ? sched_slot(di, st) : nullptr;
   if (G == 8)
-    pp_seg_kernel<8><<<g, kSegThreads, 0, st>>>(a);
+    pp_seg_kernel<8><<<g, kSegThreads, 0, st>>>(b);
   else if (G == 16)
-    pp_seg_kernel<16><<<g, kSegThreads, 0, st>>>(a);
+    pp_seg_kernel<16><<<g, kSegThreads, 0, st>>>(b);
   else
-    pp_seg_kernel<32><<<g, kSegThreads, 0, st>>>(a);
+    pp_seg_kernel<32><<<g, kSegThreads, 0, st>>>(b);
   return cudaGetLastError();
 }
 
