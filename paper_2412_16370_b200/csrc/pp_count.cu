@@ -432,15 +432,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   if (threadIdx.x == 0) PP_TL(5);
   if (kCount) fold_frame_to_counters(frame, a);
   if (threadIdx.x == 0) PP_TL(6);
-  if (a.sched && threadIdx.x == 0) {
-    // every producer of the grid has drawn its last ticket before its CTA
-    // got here: the last CTA re-arms the scheduler slot for the next launch
-    // on this stream (stream order, or griddepcontrol.wait under PDL)
-    if (atomicAdd(a.sched + 1, 1u) == gridDim.x - 1) {
-      atomicExch(a.sched, 0u);
-      atomicExch(a.sched + 1, 0u);
-    }
-  }
+  // every producer of the grid has drawn its last ticket before its CTA got here
+  if (a.sched && threadIdx.x == 0) sched_rearm(a.sched);
 }
 
 __global__ void __launch_bounds__(kLdgThreads)

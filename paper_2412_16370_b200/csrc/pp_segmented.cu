@@ -186,12 +186,9 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
       first += nw * S;
     }
   }
-  if (a.sched) {  // the last CTA re-arms the scheduler slot
+  if (a.sched) {
     __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(a.sched + 1, 1u) == gridDim.x - 1) {
-      atomicExch(a.sched, 0u);
-      atomicExch(a.sched + 1, 0u);
-    }
+    if (threadIdx.x == 0) sched_rearm(a.sched);
   }
 }
 
@@ -460,12 +457,7 @@ __global__ void __launch_bounds__(kSegTmaThreads, 1)
   }
   }
   __syncthreads();
-  if (a.sched && threadIdx.x == 0) {  // the last CTA re-arms the scheduler slot
-    if (atomicAdd(a.sched + 1, 1u) == gridDim.x - 1) {
-      atomicExch(a.sched, 0u);
-      atomicExch(a.sched + 1, 0u);
-    }
-  }
+  if (a.sched && threadIdx.x == 0) sched_rearm(a.sched);
 }
 // ------------------------------------------------------------------ host side
 cudaError_t segmented_setup(DevInfo *d) {

@@ -350,3 +350,57 @@ def test_pdl_contract_generate_then_count(cuda, oracle):
         assert [int(x) for x in cnt[i].cpu()] == oracle.hs512(host, 0, n, 16, threads=8), i
     for i in range(4):
         assert [int(x) for x in ccnt[i].cpu()] == oracle.categories(oracle.gen_codes8(n, 2000 + i), 32)
+
+
+def test_dynamic_schedule_boundaries_and_streams(cuda, oracle):
+    """The ticketed chunk order (inputs >= 4096 chunks of 32 KiB = 128 MiB):
+    lengths either side of the switch, odd offsets and tails, concurrent
+    launches on several streams (one scheduler slot per stream), a CUDA
+    graph capture of a large count (static order inside captures), and the
+    fixed-segment TMA kernel sharing a stream's slot with the count kernel."""
+    torch, pp = cuda
+    from paper_2412_16370_b200 import gen
+    n = (160 << 20) + 64
+    buf = gen.generate("uniform", n, 0xD1)
+    host = buf.cpu().numpy()
+    mib128 = 128 << 20
+    cases = [(0, mib128 - 32768), (0, mib128), (3, mib128 + 40), (16, mib128 + 32768 + 8),
+             (7, (160 << 20) - 8)]
+    for off, ln in cases:
+        want = oracle.hs512(host, off, ln, 8)
+        c = torch.zeros(8, dtype=torch.int64, device="cuda")
+        for _ in range(3):  # back to back on one stream: the slot re-arms each time
+            pp.pospopcnt(pp.InputView(buf, off, ln), 8, counters=c)
+        assert [int(x) for x in c.cpu()] == [3 * v for v in want], (off, ln)
+    # several streams at once, each with its own slot
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    outs = [torch.zeros(16, dtype=torch.int64, device="cuda") for _ in streams]
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for i, (st, o) in enumerate(zip(streams, outs)):
+            with torch.cuda.stream(st):
+                pp.pospopcnt(pp.InputView(buf, 8 * i, mib128 + 4096 * i), 16, counters=o)
+    torch.cuda.synchronize()
+    for i, o in enumerate(outs):
+        want = oracle.hs512(host, 8 * i, mib128 + 4096 * i, 16)
+        assert [int(x) for x in o.cpu()] == [3 * v for v in want], i
+    # graph capture of a large count: replays stay exact
+    c = torch.zeros(32, dtype=torch.int64, device="cuda")
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        pp.pospopcnt(pp.InputView(buf, 0, 150 << 20), 32, counters=c)
+    c.zero_()
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    assert [int(x) for x in c.cpu()] == [2 * v for v in oracle.hs512(host, 0, 150 << 20, 32)]
+    # the segmented TMA kernel and the count kernel alternating on one stream
+    rows = None
+    for _ in range(2):
+        rows = pp.pospopcnt_fixed(buf[: 160 << 20], 4096, 64)
+        c64 = torch.zeros(64, dtype=torch.int64, device="cuda")
+        pp.pospopcnt(buf[: 160 << 20], 64, counters=c64)
+    got_rows = rows.cpu().numpy().view(np.uint64)
+    assert np.array_equal(got_rows.sum(axis=0), np.array(oracle.hs512(host, 0, 160 << 20, 64),
+                                                         dtype=np.uint64))
+    assert [int(x) for x in c64.cpu()] == oracle.hs512(host, 0, 160 << 20, 64)
