@@ -39,7 +39,7 @@ def main():
     # segmented: ragged, misaligned, empty segments; last one ends at the allocation end
     for w in (8, 64):
         step = w // 8
-        for lanes in (8, 16, 32):
+        for lanes in (1, 8, 16, 32):
             lens = [rng.choice((0, step, 3 * step, 17 * step, 4096, 5000 - 5000 % step))
                     for _ in range(300)]
             offs = np.zeros(len(lens) + 1, dtype=np.int64)
@@ -52,6 +52,17 @@ def main():
             want = O.segments(host, (offs + base).astype(np.uint64), w)
             assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (w, lanes)
             checked += 1
+    # fixed segments (one lane per array below 1 KiB) ending at the allocation end
+    for seg, w in ((8, 64), (24, 8), (136, 16), (4096, 32)):
+        for off in (0, 5):
+            nseg = 777
+            host = np.frombuffer(rng.randbytes(off + nseg * seg), np.uint8)
+            buf = torch.from_numpy(host.copy()).cuda()
+            out = pp.pospopcnt_fixed(pp.InputView(buf, off, nseg * seg), seg, w)
+            want = O.segments(host, (np.arange(nseg + 1, dtype=np.uint64) * seg + off), w)
+            assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (seg, w, off)
+            checked += 1
+            del buf
     # one pass for all widths, host path
     host = np.frombuffer(rng.randbytes(4099), np.uint8)
     buf = torch.from_numpy(host.copy()).cuda()
