@@ -1,6 +1,8 @@
 #!/usr/bin/env python3
-"""Experiment: count a pinned (UVA-mapped) host buffer in place over PCIe vs
-the pipelined copy path.  PP_LIB_PATH=scripts/variants/lib_hm.so."""
+"""Experiment: count a pinned (UVA-mapped) host buffer in
+place over PCIe vs the pipelined copy path.  Needs a build whose
+check_device_ptr (csrc/pp_api.cu) also accepts cudaMemoryTypeHost pointers
+with a device mapping -- the shipped library rejects them."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
