@@ -60,6 +60,10 @@ extern "C" {
  * CSR: 32 = one warp per segment).  1 = one lane per segment (SWAR counts,
  * for arrays of a few words; a long segment then runs on a single lane). */
 #define PP_SEG_LANES(g)   ((g) << 8)
+/* CSR only, opt-in: arrays of <= 1024 bytes are counted one lane each and
+ * the longer ones with the PP_SEG_LANES shape (two launches, each row written
+ * once).  Pays for strongly bimodal lengths (profiles/r1_segmented_ablation.md). */
+#define PP_SEG_HYBRID     (1 << 16)
 
 PP_API int         pp_abi_version(void);
 PP_API const char *pp_strerror(int code);

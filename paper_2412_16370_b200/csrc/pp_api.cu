@@ -328,6 +328,8 @@ int pp_count_segmented(const void *base, const unsigned long long *seg_off, size
   a.width = width;
   a.overwrite = (flags & PP_SEG_OVERWRITE) ? 1 : 0;
   a.lanes_per_segment = seg_lanes(flags, 1ull << 20);  // unknown lengths: one warp each
+  // opt-in: tiny arrays one lane each, the rest with G lanes (two passes)
+  if ((flags & PP_SEG_HYBRID) && a.lanes_per_segment != 1) a.short_max = kLaneAutoMaxBytes;
   return seg_common(a, stream);
 }
 

@@ -39,6 +39,9 @@ struct SegArgs {
   int overwrite;
   int lanes_per_segment;  // G in {1, 8, 16, 32}
   unsigned int *sched;    // dynamic chunk scheduler slot (TMA ring kernel), or nullptr
+  // hybrid split (0 = off): segments of <= short_max bytes are counted one
+  // lane each (pp_seglane_kernel), the longer ones by the G-lane kernel
+  unsigned long long short_max;
 };
 
 enum class LoadPath : int { kTma = 0, kLdg = 1 };

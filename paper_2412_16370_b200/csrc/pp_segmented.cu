@@ -140,50 +140,64 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
   // group gw first, then (a.sched) tickets of the stream's scheduler slot,
   // one per group of S segments (group nw + ticket), else the grid stride:
   // ragged lengths no longer leave a few warps with most of the bytes
-  for (unsigned long long first = gw * S; first < a.nseg;) {
-    const unsigned long long s = first + sl;
-    const SegGeom g = seg_geom(a, s);
-    GroupCounter<G, PP_SEG_SMEM_COUNTS> c;
-    c.init(slots + (threadIdx.x >> 5) * (2 * S * 32) + lane);
-    // full (aligned, in-range) vectors are [kf0, kf1)
-    const unsigned long long kf0 = g.hp ? 1 : 0;
-    const unsigned long long kf1 = (g.tp && g.nvv) ? g.nvv - 1 : g.nvv;
-    const uint4 *vp = reinterpret_cast<const uint4 *>(g.A) + r;
-    auto load_round = [&](unsigned long long k0, uint4 (&v)[8]) {
-      if (k0 + r >= kf0 && k0 + r + 7 * G < kf1) {
-        // fast path: 8 full vectors, base pointer + immediate offsets
+  // work comes in batches of T groups (8 segments): batch gw first, then
+  // (a.sched) one ticket of the stream's scheduler slot per batch (batch
+  // nw + ticket), else the grid stride -- ragged lengths no longer leave a
+  // few warps with most of the bytes, at one atomic per 8 segments
+  constexpr unsigned T = 8 / S;
+  for (unsigned long long batch = gw;;) {
+    if (batch * T * S >= a.nseg) break;
+    for (unsigned tg = 0; tg < T; ++tg) {
+      const unsigned long long first = (batch * T + tg) * S;
+      if (first >= a.nseg) break;
+      const unsigned long long s = first + sl;
+      SegGeom g = seg_geom(a, s);
+      // hybrid split: short segments belong to the one-lane kernel
+      const bool mine = s < a.nseg && (a.short_max == 0 || g.e - g.p0 > a.short_max);
+      if (!mine) g.nvv = 0;
+      if (!__any_sync(FULL, mine)) continue;  // the whole group is short
+      GroupCounter<G, PP_SEG_SMEM_COUNTS> c;
+      c.init(slots + (threadIdx.x >> 5) * (2 * S * 32) + lane);
+      // full (aligned, in-range) vectors are [kf0, kf1)
+      const unsigned long long kf0 = g.hp ? 1 : 0;
+      const unsigned long long kf1 = (g.tp && g.nvv) ? g.nvv - 1 : g.nvv;
+      const uint4 *vp = reinterpret_cast<const uint4 *>(g.A) + r;
+      auto load_round = [&](unsigned long long k0, uint4 (&v)[8]) {
+        if (k0 + r >= kf0 && k0 + r + 7 * G < kf1) {
+          // fast path: 8 full vectors, base pointer + immediate offsets
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = ldg_stream(vp + k0 + j * G);
-      } else {
+          for (int j = 0; j < 8; ++j) v[j] = ldg_stream(vp + k0 + j * G);
+        } else {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const unsigned long long k = k0 + j * G + r;
-          v[j] = make_uint4(0u, 0u, 0u, 0u);
-          if (k < g.nvv) {
-            const uintptr_t va = g.A + 16 * k;
-            if (seg_partial(g, k))
-              v[j] = load_partial(va, g.p0, g.e);
-            else
-              v[j] = ldg_stream(reinterpret_cast<const uint4 *>(va));
+          for (int j = 0; j < 8; ++j) {
+            const unsigned long long k = k0 + j * G + r;
+            v[j] = make_uint4(0u, 0u, 0u, 0u);
+            if (k < g.nvv) {
+              const uintptr_t va = g.A + 16 * k;
+              if (seg_partial(g, k))
+                v[j] = load_partial(va, g.p0, g.e);
+              else
+                v[j] = ldg_stream(reinterpret_cast<const uint4 *>(va));
+            }
           }
         }
+      };
+      // (a software-pipelined variant that keeps the next round in flight was
+      // no faster: profiles/r1_segmented_ablation.md)
+      for (unsigned long long k0 = 0; __any_sync(FULL, k0 < g.nvv); k0 += 8 * G) {
+        uint4 v[8];
+        load_round(k0, v);
+        c.eat8(v, t);
       }
-    };
-    // (a software-pipelined variant that keeps the next round in flight was
-    // no faster: profiles/r1_segmented_ablation.md)
-    for (unsigned long long k0 = 0; __any_sync(FULL, k0 < g.nvv); k0 += 8 * G) {
-      uint4 v[8];
-      load_round(k0, v);
-      c.eat8(v, t);
+      c.finish(t);
+      if (mine) write_row(a, s, g.p0, c, lane);
     }
-    c.finish(t);
-    if (s < a.nseg) write_row(a, s, g.p0, c, lane);
     if (a.sched) {
       unsigned long long tk = 0;
       if (lane == 0) tk = atomicAdd(a.sched, 1u);
-      first = (nw + __shfl_sync(FULL, tk, 0)) * S;
+      batch = nw + __shfl_sync(FULL, tk, 0);
     } else {
-      first += nw * S;
+      batch += nw;
     }
   }
   if (a.sched) {
@@ -244,6 +258,10 @@ __global__ void __launch_bounds__(kLaneThreads)
         if (b1 < b0) b1 = b0;
       }
     }
+    // hybrid split: longer segments belong to the G-lane kernel (row untouched)
+    const bool mine = s < a.nseg && (a.short_max == 0 || b1 - b0 <= a.short_max);
+    if (!mine) b1 = b0;
+    const unsigned rows_mine = __ballot_sync(FULL, mine);
     const uintptr_t p0 = base + b0, e = base + b1;
     const int rot = 8 * (int)(p0 & 7u);
     uint32_t nl[4] = {0u, 0u, 0u, 0u}, nh[4] = {0u, 0u, 0u, 0u};
@@ -319,6 +337,7 @@ __global__ void __launch_bounds__(kLaneThreads)
     const int lw = __ffs(w) - 1;
     for (uint32_t idx = lane; idx < nrows * (uint32_t)w; idx += 32) {
       const uint32_t r = idx >> lw, j = idx & (uint32_t)(w - 1);
+      if (!((rows_mine >> r) & 1u)) continue;
       unsigned long long val = 0ull;
       for (int i = (int)j; i < 64; i += w) val += fr[i * kLaneStride + r];
       dst[idx] = a.overwrite ? val : dst[idx] + val;
@@ -501,6 +520,13 @@ static bool seg_use_tma(const SegArgs &a, const DevInfo &di, unsigned *items_per
 cudaError_t launch_segmented(const SegArgs &a, const DevInfo &di, cudaStream_t st) {
   if (a.nseg == 0) return cudaSuccess;
   const int G = a.lanes_per_segment;
+  if (a.short_max && G != 1) {
+    // hybrid: short segments one lane each, then the rest with G lanes
+    SegArgs sh = a;
+    sh.lanes_per_segment = 1;
+    cudaError_t e = launch_segmented(sh, di, st);
+    if (e != cudaSuccess) return e;
+  }
   if (G == 1) {  // one lane per segment
     const unsigned long long need = (a.nseg + kLaneThreads - 1) / kLaneThreads;
     const unsigned g = grid_for(need, (unsigned long long)di.num_sms * di.lane_blocks_per_sm);

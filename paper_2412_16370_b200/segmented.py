@@ -44,7 +44,7 @@ def _out_tensor(out, nseg, width, device):
 
 
 def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validate=True,
-                        lanes=None):
+                        lanes=None, hybrid=False):
     """Positional counts of many arrays in one launch.
 
     ``offsets``: nseg+1 non-decreasing byte offsets into the view (host
@@ -52,15 +52,20 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
     (nseg, width) int64 tensor accumulated into (or overwritten when
     ``accumulate=False``); allocated zeroed when None.  Returns ``out``.
     Asynchronous on the current stream.  ``lanes`` (1, 8, 16 or 32) forces
-    the lanes-per-segment launch shape; by default it follows the segment
-    lengths when the offsets are on the host (1 when every segment is at most
-    LANE_MAX_BYTES).
+    the lanes-per-segment launch shape.  By default it follows the segment
+    lengths (host offsets, or device offsets with ``validate``): one lane per
+    segment when every segment is at most LANE_MAX_BYTES, else G lanes by the
+    mean length; unknown lengths (device offsets, ``validate=False``) get the
+    C ABI default, G = 32.  ``hybrid=True`` adds a one-lane pass for the
+    segments of at most LANE_MAX_BYTES (PP_SEG_HYBRID), which pays for
+    strongly bimodal lengths.
     """
     import torch
     check_width(width)
     view = _device_view(data)
     dev = view.base.device
     step = width // 8
+    shape = None  # (lanes, hybrid) from the lengths, when they are known here
     if is_torch_tensor(offsets) and offsets.is_cuda:
         offs = offsets.to(torch.int64).contiguous()
         if validate and offs.numel() > 1:
@@ -71,10 +76,8 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
             if bool((d % step != 0).any()):
                 raise InputLengthError(f"a segment is not a multiple of the {step}-byte word size")
             if lanes is None:  # validation already synchronised: pick the shape too
-                dmax, total = int(d.max()), int(offs[-1] - offs[0])
-                mean = total // d.numel()
-                lanes = (1 if dmax <= LANE_MAX_BYTES else
-                         32 if mean >= 16384 else 16 if mean >= 8192 else 8)
+                nlong = int((d > LANE_MAX_BYTES).sum())
+                shape = _shape(int(d.numel()), nlong, int(offs[-1] - offs[0]) // d.numel())
     else:
         offs_np = np.asarray(offsets, dtype=np.int64)
         if offs_np.ndim != 1 or offs_np.size < 1:
@@ -88,17 +91,18 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
         offs = torch.as_tensor(offs_np, device=dev)
         if lanes is None and offs_np.size > 1:
             d = np.diff(offs_np)
-            mean = (int(offs_np[-1]) - int(offs_np[0])) // (offs_np.size - 1)
-            # one lane per array when every array is tiny (no long outlier
-            # can stall a lane), else G lanes by the mean length
-            lanes = (1 if int(d.max()) <= LANE_MAX_BYTES else
-                     32 if mean >= 16384 else 16 if mean >= 8192 else 8)
+            nlong = int((d > LANE_MAX_BYTES).sum())
+            shape = _shape(int(d.size), nlong, (int(offs_np[-1]) - int(offs_np[0])) // d.size)
     nseg = offs.numel() - 1
     out, fresh = _out_tensor(out, max(nseg, 0), width, dev)
     if nseg <= 0:
         return out
     lib = _lib.load()
     flags = _lib.PP_SEG_ACCUMULATE if (accumulate and not fresh) else _lib.PP_SEG_OVERWRITE
+    if lanes is None and shape is not None:
+        lanes = shape[0]
+    if hybrid:
+        flags |= _lib.PP_SEG_HYBRID
     flags |= _lanes_flag(lanes)
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream(dev).cuda_stream
@@ -108,6 +112,19 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
         # keep the offsets tensor alive until the kernel has consumed it
         offs.record_stream(torch.cuda.current_stream(dev))
     return out
+
+
+def _shape(nseg, nlong, mean):
+    """Launch shape from the length distribution: (lanes, hybrid).
+
+    Every array <= LANE_MAX_BYTES: one lane each, else G lanes by the mean
+    length.  The hybrid split (PP_SEG_HYBRID, short arrays one lane each in a
+    separate pass) is opt-in: measured, it wins only for strongly bimodal
+    lengths (profiles/r1_segmented_ablation.md).
+    """
+    if nlong == 0:
+        return 1, False
+    return (32 if mean >= 16384 else 16 if mean >= 8192 else 8), False
 
 
 def _lanes_flag(lanes):

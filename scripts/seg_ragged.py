@@ -22,9 +22,9 @@ for name, mk in cases.items():
     offs[1:] = np.cumsum(lens)
     d = torch.from_numpy(offs).cuda()
     nseg = lens.size
-    for lanes in (8, 32):
+    for lanes, extra in ((8, 0), (32, 0), (8, _lib.PP_SEG_HYBRID), (16, _lib.PP_SEG_HYBRID), (0, 0)):
         out = torch.zeros((nseg, 64), dtype=torch.int64, device="cuda")
-        f = lambda: _lib.check(lib.pp_count_segmented(buf.data_ptr(), d.data_ptr(), nseg, 64, out.data_ptr(), 1 | (lanes << 8), sp))
+        f = lambda: _lib.check(lib.pp_count_segmented(buf.data_ptr(), d.data_ptr(), nseg, 64, out.data_ptr(), 1 | (lanes << 8) | extra, sp))
         for _ in range(3):
             f()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -34,4 +34,4 @@ for name, mk in cases.items():
         b.record(); torch.cuda.synchronize()
         us = a.elapsed_time(b) / 10 * 1e3
         tot = int(offs[-1]) + nseg * 512
-        print(f"{tag} {name} nseg={nseg} lanes={lanes} us={us:.1f} inout_GBs={tot / us / 1e3:.0f}", flush=True)
+        print(f"{tag} {name} nseg={nseg} lanes={lanes}{'+hybrid' if extra else ''} us={us:.1f} inout_GBs={tot / us / 1e3:.0f}", flush=True)

@@ -50,7 +50,10 @@ def test_c1_exhaustive_sweep_via_segments(cuda, oracle):
         buf = torch.from_numpy(host).cuda()
         doffs = torch.from_numpy(offs).cuda()
         got = None
-        for lanes, path in ((32, 0), (16, 0), (8, 0), (1, 0)):
+        # (lanes hint, extra flags): every shape, the default (0 = G 32), and
+        # the hybrid split (short arrays one lane each) with two shapes
+        for lanes, path in ((32, 0), (16, 0), (8, 0), (1, 0), (0, 0), (8, _lib.PP_SEG_HYBRID),
+                            (32, _lib.PP_SEG_HYBRID)):
             # every launch shape must agree
             out = torch.zeros((3 * len(cases), w), dtype=torch.int64, device="cuda")
             rc = lib.pp_count_segmented(buf.data_ptr(), doffs.data_ptr(), 3 * len(cases), w,
@@ -90,6 +93,9 @@ def test_ragged_random_segments_poison(cuda, oracle, rng, lanes):
         out = pp.pospopcnt_segmented(view, offs, w, lanes=lanes)
         want = oracle.segments(host, (offs + base).astype(np.uint64), w)
         assert np.array_equal(out.cpu().numpy().view(np.uint64), want), w
+        if lanes in (None, 8):  # the hybrid split over the same mixed lengths
+            hy = pp.pospopcnt_segmented(view, offs, w, lanes=lanes, hybrid=True)
+            assert np.array_equal(hy.cpu().numpy().view(np.uint64), want), w
         # accumulate semantics
         pp.pospopcnt_segmented(view, offs, w, out=out, lanes=lanes)
         assert np.array_equal(out.cpu().numpy().view(np.uint64), 2 * want), w
