@@ -8,8 +8,11 @@ point takes the codes themselves and returns exactly
                                       == #{i : codes[i] == j}
 
 without materialising the w/8-byte one-hot words (codes >= w have no bit in a
-w-bit word and are not counted).  Computed by pp_count_categories
-(csrc/pp_categories.cu).
+w-bit word and are not counted; negative 2-/4-byte codes neither).  Computed
+by pp_count_categories: the codes (1, 2 or 4 bytes each) are expanded into
+packed one-hot words in registers on the TMA pipeline and counted by the
+same carry-save counter as pospopcnt (csrc/pp_count.cu; the shared-memory
+histogram of csrc/pp_categories.cu remains as the A/B alternative).
 """
 
 import numpy as np

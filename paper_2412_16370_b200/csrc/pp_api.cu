@@ -262,23 +262,23 @@ int pp_count_categories(const void *codes, size_t ncodes, int code_bytes, int wi
   int dev = 0;
   cudaGetDevice(&dev);
   cudaError_t e;
-  // u8 codes: one-hot expansion on the TMA pipeline (faster at every width,
-  // profiles/r1_categories_ablation.md); 2- / 4-byte codes: shared-memory
-  // histogram columns.  PP_CAT_PATH=smem|onehot forces a path (A/B runs).
+  // One-hot expansion on the TMA pipeline at every code width (faster than
+  // the shared-memory histogram everywhere: profiles/r1_categories_ablation.md).
+  // PP_CAT_PATH=smem|onehot forces a path (A/B runs).
   const char *force = std::getenv("PP_CAT_PATH");
   const bool onehot = force ? std::strcmp(force, "onehot") == 0 : true;
-  if (code_bytes == 1 && onehot) {
-    // u8 codes: expand to packed one-hot words in registers and run the
-    // carry-save counter on the TMA pipeline (frame position = code mod w)
+  if (onehot) {
+    // expand to packed one-hot words in registers and run the carry-save
+    // counter on the TMA pipeline (frame position = code mod w)
     pp::CountArgs a{};
-    pp::split_range(static_cast<const uint8_t *>(codes), ncodes, pp::codes8_chunk_bytes(), &a);
+    pp::split_range(static_cast<const uint8_t *>(codes), (unsigned long long)ncodes * code_bytes,
+                    pp::codes8_chunk_bytes(), &a);
     a.counters = counters;
     a.width = width;
     a.rot = 0;
-    e = pp::launch_count_codes8(a, di, static_cast<cudaStream_t>(stream));
+    e = pp::launch_count_codes(a, code_bytes, di, static_cast<cudaStream_t>(stream));
   } else {
-    // 2- / 4-byte codes (and the A/B alternative for u8): per-thread shared
-    // memory histogram columns
+    // the A/B alternative: per-thread shared-memory histogram columns
     e = pp::launch_categories(static_cast<const uint8_t *>(codes),
                               (unsigned long long)ncodes * code_bytes, code_bytes, width,
                               counters, di, dev, static_cast<cudaStream_t>(stream));

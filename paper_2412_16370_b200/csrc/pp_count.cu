@@ -259,17 +259,111 @@ __device__ __forceinline__ void eat_codes(Counter &c, const uint4 (&v)[8], uint3
   }
 }
 
-// Head/tail codes (< 16 each) of the fused producer: frame position = code.
+// 2- / 4-byte codes (CB = code bytes): the same packed one-hot words, built
+// from wider lanes.  shl clamps any shift amount >= the register width to a
+// zero result, so codes >= W need no test however large they are; the
+// byte/half masks drop the rest.  Words of absent vectors (partial chunk)
+// must be zero, not "code 0".
+__device__ __forceinline__ uint32_t shl32(uint32_t x, uint32_t n) {
+  uint32_t r;
+  asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(n));
+  return r;
+}
+// codes c0..c3 -> byte k = one-hot8(c_k) (c_k < 8)
+__device__ __forceinline__ uint32_t oh8quad(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
+  return (shl32(1u, c0) & 0xFFu) | (shl32(0x100u, c1) & 0xFF00u) |
+         (shl32(0x10000u, c2) & 0xFF0000u) | shl32(0x1000000u, c3);
+}
+// codes c0, c1 -> half k = one-hot16(c_k) (c_k < 16)
+__device__ __forceinline__ uint32_t oh16pair(uint32_t c0, uint32_t c1) {
+  return (shl32(1u, c0) & 0xFFFFu) | shl32(0x10000u, c1);
+}
+
+template <int W, bool FULL, int CB>
+__device__ __forceinline__ void eat_wide_codes(Counter &c, const uint4 (&v)[8], uint32_t valid,
+                                               const TC &t) {
+  static_assert(CB == 2 || CB == 4, "code bytes");
+  const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+  // this thread's K codes, in order: vector i holds 16 / CB of them
+  constexpr int K = 8 * 16 / CB;
+  auto code = [&](int k) -> uint32_t {
+    const uint4 x = v[k / (16 / CB)];
+    const int j = k % (16 / CB);
+    const uint32_t wd = (CB == 4) ? (j == 0 ? x.x : j == 1 ? x.y : j == 2 ? x.z : x.w)
+                                  : (j / 2 == 0 ? x.x : j / 2 == 1 ? x.y : j / 2 == 2 ? x.z : x.w);
+    return CB == 4 ? wd : (j & 1 ? wd >> 16 : wd & 0xFFFFu);
+  };
+  auto present = [&](int k) -> bool { return FULL || ((valid >> (k / (16 / CB))) & 1u); };
+  if (W == 32) {  // one word per code: K / 32 rounds
+#pragma unroll
+    for (int r = 0; r < K / 32; ++r) {
+      uint4 u[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int k = 32 * r + 4 * q;
+        u[q] = present(k) ? make_uint4(shl32(1u, code(k)), shl32(1u, code(k + 1)),
+                                       shl32(1u, code(k + 2)), shl32(1u, code(k + 3)))
+                          : z4;
+      }
+      c.eat8(u, t);
+    }
+  } else if (W == 64) {  // one (lo, hi) pair per code: K / 16 rounds
+#pragma unroll
+    for (int r = 0; r < K / 16; ++r) {
+      uint4 u[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int k = 16 * r + 2 * q;
+        uint32_t l0, h0, l1, h1;
+        onehot64(code(k), l0, h0);
+        onehot64(code(k + 1), l1, h1);
+        u[q] = present(k) ? make_uint4(l0, h0, l1, h1) : z4;
+      }
+      c.eat8(u, t);
+    }
+  } else {  // W = 16: two codes per word, W = 8: four; one round, padded
+    constexpr int PER = W == 16 ? 2 : 4;
+    constexpr int NW = K / PER;  // packed words (<= 32)
+    uint4 u[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      uint32_t wq[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int n = 4 * q + e;  // packed word index
+        const int k = PER * n;
+        if (n >= NW || !present(k)) {
+          wq[e] = 0u;
+        } else if (W == 16) {
+          wq[e] = oh16pair(code(k), code(k + 1));
+        } else {
+          wq[e] = oh8quad(code(k), code(k + 1), code(k + 2), code(k + 3));
+        }
+      }
+      u[q] = make_uint4(wq[0], wq[1], wq[2], wq[3]);
+    }
+    c.eat8(u, t);
+  }
+}
+
+// Head/tail codes (< 16 bytes each) of the fused producer: frame position =
+// code.  Lane l < 16 takes head code l, lane 16 + l tail code l.
+template <int CB>
 __device__ __forceinline__ void count_code_edges(Counter &c, const uint8_t *head, uint32_t hb,
                                                  const uint8_t *tail, uint32_t tb, uint32_t lane,
                                                  int width, const TC &t) {
-  uint32_t code = 0xFFu;
+  uint32_t code = 0xFFFFFFFFu;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // input complete (PDL)
+  const uint8_t *p = nullptr;
   if (lane < 16) {
-    if (lane < hb) code = __ldg(head + lane);
-  } else if (lane - 16 < tb) {
-    code = __ldg(tail + (lane - 16));
+    if (lane < hb / CB) p = head + CB * lane;
+  } else if (lane - 16 < tb / CB) {
+    p = tail + CB * (lane - 16);
   }
+  if (p)
+    code = CB == 1 ? __ldg(p)
+                   : CB == 2 ? __ldg(reinterpret_cast<const uint16_t *>(p))
+                             : __ldg(reinterpret_cast<const uint32_t *>(p));
   const bool ok = code < (uint32_t)width;
   c.ce += wcount(ok ? onehot32(code) : 0u, t);
   c.co += wcount(ok ? onehot32(code - 32u) : 0u, t);
@@ -296,8 +390,8 @@ __device__ __forceinline__ unsigned long long gtime() {
 #endif
 
 // MODE 0: read-only roofline (XOR of every word), MODE 1: positional count,
-// MODE 8/16/32/64: fused one-hot producer over u8 codes at that width.
-template <int MODE, int NCW = kTmaConsumerWarps>
+// MODE 8/16/32/64: fused one-hot producer over CB-byte codes at that width.
+template <int MODE, int NCW = kTmaConsumerWarps, int CB = 1>
 __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     pp_tma_kernel(CountArgs a, unsigned long long *sink) {
   constexpr bool kCount = MODE != 0;
@@ -395,11 +489,16 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       if (lane == 0) mbar_arrive(&empty[stage]);
       if (MODE == 1) {
         c.eat8(v, t);
-      } else if (MODE >= 8) {
+      } else if (MODE >= 8 && CB == 1) {
         if (valid == 0xFFu)
           eat_codes<(MODE >= 8 ? MODE : 8), true>(c, v, valid, t);
         else
           eat_codes<(MODE >= 8 ? MODE : 8), false>(c, v, valid, t);
+      } else if (MODE >= 8) {
+        if (valid == 0xFFu)
+          eat_wide_codes<(MODE >= 8 ? MODE : 8), true, (CB > 1 ? CB : 2)>(c, v, valid, t);
+        else
+          eat_wide_codes<(MODE >= 8 ? MODE : 8), false, (CB > 1 ? CB : 2)>(c, v, valid, t);
       } else {
 #pragma unroll
         for (int i = 0; i < 8; ++i) xs ^= v[i].x ^ v[i].y ^ v[i].z ^ v[i].w;
@@ -416,7 +515,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         if (MODE == 1)
           count_edges(c, a.head, a.head_bytes, a.tail, a.tail_bytes, lane, t);
         else
-          count_code_edges(c, a.head, a.head_bytes, a.tail, a.tail_bytes, lane, a.width, t);
+          count_code_edges<CB>(c, a.head, a.head_bytes, a.tail, a.tail_bytes, lane, a.width, t);
       }
       atomicAdd(&frame[lane], c.ce);
       atomicAdd(&frame[32 + lane], c.co);
@@ -508,7 +607,11 @@ static cudaError_t compute_device_info(int dev, DevInfo *out) {
                                 (int)kTmaSmemBytes)))
     return e;
   for (auto k : {pp_tma_kernel<8, PP_CAT_NCW>, pp_tma_kernel<16, PP_CAT_NCW>,
-                 pp_tma_kernel<32, PP_CAT_NCW>, pp_tma_kernel<64, PP_CAT_NCW>})
+                 pp_tma_kernel<32, PP_CAT_NCW>, pp_tma_kernel<64, PP_CAT_NCW>,
+                 pp_tma_kernel<8, PP_CAT_NCW, 2>, pp_tma_kernel<16, PP_CAT_NCW, 2>,
+                 pp_tma_kernel<32, PP_CAT_NCW, 2>, pp_tma_kernel<64, PP_CAT_NCW, 2>,
+                 pp_tma_kernel<8, PP_CAT_NCW, 4>, pp_tma_kernel<16, PP_CAT_NCW, 4>,
+                 pp_tma_kernel<32, PP_CAT_NCW, 4>, pp_tma_kernel<64, PP_CAT_NCW, 4>})
     if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)CatShape::kSmem)))
       return e;
@@ -643,23 +746,30 @@ cudaError_t launch_count(const CountArgs &a, LoadPath path, const DevInfo &di,
   return cudaGetLastError();
 }
 
-cudaError_t launch_count_codes8(const CountArgs &a, const DevInfo &di, cudaStream_t st) {
+template <int CB>
+static cudaError_t launch_codes(const CountArgs &a, const DevInfo &di, cudaStream_t st) {
   const unsigned g = grid_for(a.nchunks, (unsigned long long)di.count_sms);
   switch (a.width) {
     case 8:
-      return launch_tma(pp_tma_kernel<8, PP_CAT_NCW>, g, CatShape::kThreads, CatShape::kSmem, st,
-                        a, nullptr, true, di);
+      return launch_tma(pp_tma_kernel<8, PP_CAT_NCW, CB>, g, CatShape::kThreads, CatShape::kSmem,
+                        st, a, nullptr, true, di);
     case 16:
-      return launch_tma(pp_tma_kernel<16, PP_CAT_NCW>, g, CatShape::kThreads, CatShape::kSmem,
-                        st, a, nullptr, true, di);
+      return launch_tma(pp_tma_kernel<16, PP_CAT_NCW, CB>, g, CatShape::kThreads,
+                        CatShape::kSmem, st, a, nullptr, true, di);
     case 32:
-      return launch_tma(pp_tma_kernel<32, PP_CAT_NCW>, g, CatShape::kThreads, CatShape::kSmem,
-                        st, a, nullptr, true, di);
+      return launch_tma(pp_tma_kernel<32, PP_CAT_NCW, CB>, g, CatShape::kThreads,
+                        CatShape::kSmem, st, a, nullptr, true, di);
     default:
-      return launch_tma(pp_tma_kernel<64, PP_CAT_NCW>, g, CatShape::kThreads, CatShape::kSmem,
-                        st, a, nullptr, true, di);
+      return launch_tma(pp_tma_kernel<64, PP_CAT_NCW, CB>, g, CatShape::kThreads,
+                        CatShape::kSmem, st, a, nullptr, true, di);
   }
-  return cudaGetLastError();
+}
+
+cudaError_t launch_count_codes(const CountArgs &a, int code_bytes, const DevInfo &di,
+                               cudaStream_t st) {
+  return code_bytes == 1   ? launch_codes<1>(a, di, st)
+         : code_bytes == 2 ? launch_codes<2>(a, di, st)
+                           : launch_codes<4>(a, di, st);
 }
 
 cudaError_t launch_readonly(const CountArgs &a, unsigned long long *sink, const DevInfo &di,

@@ -81,8 +81,9 @@ unsigned long long codes8_chunk_bytes();
 cudaError_t launch_count(const CountArgs &a, LoadPath path, const DevInfo &di,
                          cudaStream_t st);
 cudaError_t launch_segmented(const SegArgs &a, const DevInfo &di, cudaStream_t st);
-// fused one-hot producer over u8 codes (a.width = W, a.rot ignored)
-cudaError_t launch_count_codes8(const CountArgs &a, const DevInfo &di, cudaStream_t st);
+// fused one-hot producer over 1/2/4-byte codes (a.width = W, a.rot ignored)
+cudaError_t launch_count_codes(const CountArgs &a, int code_bytes, const DevInfo &di,
+                               cudaStream_t st);
 cudaError_t launch_readonly(const CountArgs &a, unsigned long long *sink,
                             const DevInfo &di, cudaStream_t st);
 

@@ -73,6 +73,31 @@ def test_every_u8_code_at_every_byte_position(cuda, oracle):
             assert pp.pospopcnt_categories(codes, w) == oracle.categories(host, w), (w, host.size)
 
 
+@pytest.mark.parametrize("dtype", ("int16", "uint16", "int32", "uint32"))
+def test_wide_codes_boundaries_every_lane(cuda, oracle, dtype):
+    """2- and 4-byte codes on the one-hot TMA path: boundary values (w - 1,
+    w, 7, 8, 15, 16, 31, 32, 63, 64, the type's max, negatives) in every
+    code slot of the 16-byte vectors, mixed with uniform codes, partial
+    chunks and an unaligned (but code-aligned) start."""
+    torch, pp = cuda
+    rng = np.random.default_rng(123)
+    info = np.iinfo(dtype)
+    special = np.array([0, 1, 7, 8, 15, 16, 31, 32, 63, 64, 65, 255, 256, 1000,
+                        info.max, info.max - 1] + ([-1, -2, info.min] if info.min < 0 else []),
+                       dtype=np.int64).astype(dtype)
+    per_vec = 16 // np.dtype(dtype).itemsize
+    ex = np.concatenate([np.roll(special, k) for k in range(per_vec + 1)])
+    small = rng.integers(0, 8, 4099).astype(dtype)
+    uni = rng.integers(0, 80, (1 << 21) + 5).astype(dtype)
+    host = np.concatenate([ex, small, uni, ex])
+    aligned = torch.from_numpy(host.copy()).cuda()
+    shifted = torch.from_numpy(np.concatenate([np.zeros(3, dtype), host])).cuda()[3:]
+    for codes in (aligned, shifted, aligned[: ex.size + 5]):
+        want = host[: codes.numel()]
+        for w in (8, 16, 32, 64):
+            assert pp.pospopcnt_categories(codes, w) == oracle.categories(want, w), (w, codes.numel())
+
+
 def test_u16_column_split_across_launches(cuda):
     """Every code in one bin: each thread's u16 column sits at its 65535 limit
     and the launch is split; the total must still be exact."""
