@@ -98,9 +98,10 @@ def test_wide_codes_boundaries_every_lane(cuda, oracle, dtype):
             assert pp.pospopcnt_categories(codes, w) == oracle.categories(want, w), (w, codes.numel())
 
 
-def test_u16_column_split_across_launches(cuda):
-    """Every code in one bin: each thread's u16 column sits at its 65535 limit
-    and the launch is split; the total must still be exact."""
+def test_one_bin_past_2_32(cuda):
+    """Every code in one bin, 10 GiB of them: that counter passes 2^32 (u64
+    all the way; on the PP_CAT_PATH=smem alternative each thread's u16 column
+    sits at its 65535 limit and the launch is split)."""
     torch, pp = cuda
     n = (10 << 30) + 5
     codes = torch.full((n,), 7, dtype=torch.uint8, device="cuda")
@@ -119,3 +120,27 @@ def test_errors(cuda):
     with pytest.raises(ValueError):
         pp.pospopcnt_categories(torch.zeros(4, dtype=torch.uint8, device="cuda"), 16,
                                 counters=[0] * 8)
+
+
+def test_histogram_alternative_path(cuda):
+    """PP_CAT_PATH=smem (the shared-memory histogram, kept for A/B runs) must
+    stay exact too; the path is chosen once per process, so in a child."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    child = (
+        "import sys, numpy as np, torch\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "from oracle import oracle as O\n"
+        "import paper_2412_16370_b200 as pp\n"
+        "rng = np.random.default_rng(5)\n"
+        "for dt in ('uint8', 'int16', 'int32'):\n"
+        "    host = rng.integers(-3 if dt != 'uint8' else 0, 90, 3_000_017).astype(dt)\n"
+        "    codes = torch.from_numpy(host).cuda()\n"
+        "    for w in (8, 16, 32, 64):\n"
+        "        assert pp.pospopcnt_categories(codes, w) == O.categories(host, w), (dt, w)\n"
+        "print('ok')\n")
+    env = dict(os.environ, PP_CAT_PATH="smem")
+    res = subprocess.run([sys.executable, "-c", child], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert res.returncode == 0 and res.stdout.strip().endswith("ok"), res.stdout + res.stderr
