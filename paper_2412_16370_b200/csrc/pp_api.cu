@@ -290,14 +290,19 @@ int pp_count_categories(const void *codes, size_t ncodes, int code_bytes, int wi
 // Lanes per segment: explicit hint in flags bits 8-15, else from the
 // (average) segment size: one warp per segment from 16 KiB up, 8 lanes
 // (4 segments per warp, 4x fewer transposes per segment) below 8 KiB.
-// Lanes per segment: the hint (1, 8, 16 or 32), else from the segment length:
-// one lane each for tiny fixed segments (SWAR kernel), else G-lane groups.
-static constexpr unsigned long long kLaneAutoMaxBytes = 1024;  // crossover: scripts/seg_small.py
+// Lanes per segment: the hint (1, 2, 4, 8, 16 or 32), else from the segment
+// length: one lane each for tiny segments (SWAR kernel), else G-lane groups.
+// Crossover (scripts/seg_smallG.py): the one-lane kernel wins up to 512 B,
+// and up to 1 KiB when segments start/end inside 16-byte vectors (the G-lane
+// kernels then assemble partial vectors byte by byte); aligned 1 KiB
+// segments are 1.75x faster with G = 8.
+static constexpr unsigned long long kLaneAutoMaxBytes = 1024;
+static constexpr unsigned long long kLaneAutoMaxAligned = 512;
 
-static int seg_lanes(int flags, unsigned long long avg_bytes) {
+static int seg_lanes(int flags, unsigned long long avg_bytes, bool vec_aligned = false) {
   const int hint = (flags >> 8) & 0xFF;
-  if (hint == 1 || hint == 8 || hint == 16 || hint == 32) return hint;
-  if (avg_bytes <= kLaneAutoMaxBytes) return 1;
+  if (hint == 1 || hint == 2 || hint == 4 || hint == 8 || hint == 16 || hint == 32) return hint;
+  if (avg_bytes <= (vec_aligned ? kLaneAutoMaxAligned : kLaneAutoMaxBytes)) return 1;
   if (avg_bytes >= 16384) return 32;
   if (avg_bytes >= 8192) return 16;
   return 8;
@@ -346,7 +351,8 @@ int pp_count_fixed(const void *base, size_t seg_bytes, size_t nseg, int width,
   a.out = out;
   a.width = width;
   a.overwrite = (flags & PP_SEG_OVERWRITE) ? 1 : 0;
-  a.lanes_per_segment = seg_lanes(flags, seg_bytes);
+  a.lanes_per_segment =
+      seg_lanes(flags, seg_bytes, ((uintptr_t)base % 16 == 0) && (seg_bytes % 16 == 0));
   return seg_common(a, stream);
 }
 

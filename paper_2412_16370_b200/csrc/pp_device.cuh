@@ -216,12 +216,16 @@ __device__ __forceinline__ uint32_t gtranspose(uint32_t x, const TC &t) {
     y = __shfl_xor_sync(FULL, x, 8);
     x = __byte_perm(x, y, t.sel8);
   }
-  y = __shfl_xor_sync(FULL, x, 4);
-  y = __funnelshift_r(y, y, t.rot4);
-  x = (x & t.keep4) | (y & ~t.keep4);
-  y = __shfl_xor_sync(FULL, x, 2);
-  y = __funnelshift_r(y, y, t.rot2);
-  x = (x & t.keep2) | (y & ~t.keep2);
+  if (G > 4) {
+    y = __shfl_xor_sync(FULL, x, 4);
+    y = __funnelshift_r(y, y, t.rot4);
+    x = (x & t.keep4) | (y & ~t.keep4);
+  }
+  if (G > 2) {
+    y = __shfl_xor_sync(FULL, x, 2);
+    y = __funnelshift_r(y, y, t.rot2);
+    x = (x & t.keep2) | (y & ~t.keep2);
+  }
   y = __shfl_xor_sync(FULL, x, 1);
   y = __funnelshift_r(y, y, t.rot1);
   x = (x & t.keep1) | (y & ~t.keep1);
@@ -234,7 +238,7 @@ __device__ __forceinline__ uint32_t gtranspose(uint32_t x, const TC &t) {
 // per SM stay resident (more loads in flight).
 template <int G, bool SMEM = false>
 struct GroupCounter {
-  static_assert(G == 8 || G == 16 || G == 32, "lanes per segment");
+  static_assert(G == 2 || G == 4 || G == 8 || G == 16 || G == 32, "lanes per segment");
   static constexpr int S = 32 / G;  // positions per lane per tree
   Planes l1e, l1o, l2e, l2o;
   uint32_t l2n;
@@ -263,7 +267,7 @@ struct GroupCounter {
 
   static __device__ __forceinline__ uint32_t field_popc(uint32_t x, int f) {
     if (G == 32) return __popc(x);
-    return __popc(x & ((G == 16 ? 0xFFFFu : 0xFFu) << (f * G)));
+    return __popc(x & (((1u << G) - 1u) << (f * G)));
   }
 
   // Count the first np planes (weights 1,2,4,8 << shift) of both trees.

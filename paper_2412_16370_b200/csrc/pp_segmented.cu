@@ -128,7 +128,7 @@ __device__ __forceinline__ void write_row(const SegArgs &a, unsigned long long s
 // vectors r, r+G, ... in groups of 8 (G x 16 contiguous bytes per load
 // instruction per segment).  A TMA-fed variant (per-warp bulk-copy rings) was
 // 1.5x slower here: profiles/r1_segmented_ablation.md.
-template <int G>
+template <int G, bool HYBRID = false>
 __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
     pp_seg_kernel(SegArgs a) {
   constexpr int S = 32 / G;
@@ -152,10 +152,12 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
       if (first >= a.nseg) break;
       const unsigned long long s = first + sl;
       SegGeom g = seg_geom(a, s);
-      // hybrid split: short segments belong to the one-lane kernel
-      const bool mine = s < a.nseg && (a.short_max == 0 || g.e - g.p0 > a.short_max);
-      if (!mine) g.nvv = 0;
-      if (!__any_sync(FULL, mine)) continue;  // the whole group is short
+      bool mine = s < a.nseg;
+      if (HYBRID) {  // short segments belong to the one-lane kernel
+        mine = mine && g.e - g.p0 > a.short_max;
+        if (!mine) g.nvv = 0;
+        if (!__any_sync(FULL, mine)) continue;  // the whole group is short
+      }
       GroupCounter<G, PP_SEG_SMEM_COUNTS> c;
       c.init(slots + (threadIdx.x >> 5) * (2 * S * 32) + lane);
       // full (aligned, in-range) vectors are [kf0, kf1)
@@ -232,7 +234,7 @@ __device__ __forceinline__ uint32_t byte_range_mask(int q, int lo, int hi) {
   return m1 & m2;
 }
 
-template <bool FIXED>
+template <bool FIXED, bool HYBRID = false>
 __global__ void __launch_bounds__(kLaneThreads)
     pp_seglane_kernel(SegArgs a) {
   __shared__ uint32_t frs[kLaneWarps][64 * kLaneStride];
@@ -258,10 +260,15 @@ __global__ void __launch_bounds__(kLaneThreads)
         if (b1 < b0) b1 = b0;
       }
     }
-    // hybrid split: longer segments belong to the G-lane kernel (row untouched)
-    const bool mine = s < a.nseg && (a.short_max == 0 || b1 - b0 <= a.short_max);
-    if (!mine) b1 = b0;
-    const unsigned rows_mine = __ballot_sync(FULL, mine);
+    // hybrid split: longer segments belong to the G-lane kernel (row
+    // untouched).  A template parameter: the plain kernel must not carry this
+    // test (it cost the per-vector loop ~40 % at 1 KiB segments)
+    unsigned rows_mine = FULL;
+    if (HYBRID) {
+      const bool mine = s < a.nseg && b1 - b0 <= a.short_max;
+      if (!mine) b1 = b0;
+      rows_mine = __ballot_sync(FULL, mine);
+    }
     const uintptr_t p0 = base + b0, e = base + b1;
     const int rot = 8 * (int)(p0 & 7u);
     uint32_t nl[4] = {0u, 0u, 0u, 0u}, nh[4] = {0u, 0u, 0u, 0u};
@@ -481,7 +488,8 @@ __global__ void __launch_bounds__(kSegTmaThreads, 1)
 // ------------------------------------------------------------------ host side
 cudaError_t segmented_setup(DevInfo *d) {
   cudaError_t e;
-  for (auto k : {pp_segtma_kernel<8>, pp_segtma_kernel<16>, pp_segtma_kernel<32>})
+  for (auto k : {pp_segtma_kernel<2>, pp_segtma_kernel<4>, pp_segtma_kernel<8>,
+                 pp_segtma_kernel<16>, pp_segtma_kernel<32>})
     if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSegTmaSmem)))
       return e;
@@ -517,8 +525,14 @@ static bool seg_use_tma(const SegArgs &a, const DevInfo &di, unsigned *items_per
   return true;
 }
 
-cudaError_t launch_segmented(const SegArgs &a, const DevInfo &di, cudaStream_t st) {
-  if (a.nseg == 0) return cudaSuccess;
+cudaError_t launch_segmented(const SegArgs &a0, const DevInfo &di, cudaStream_t st) {
+  if (a0.nseg == 0) return cudaSuccess;
+  SegArgs a = a0;
+  unsigned ipc = 0;
+  // G = 2 / 4 (1-2 KiB fixed segments: 32 vectors per lane) exist only on the
+  // TMA ring; elsewhere their segments go one lane each (G = 2) or to G = 8
+  if ((a.lanes_per_segment == 2 || a.lanes_per_segment == 4) && !seg_use_tma(a, di, &ipc))
+    a.lanes_per_segment = a.lanes_per_segment == 2 ? 1 : 8;
   const int G = a.lanes_per_segment;
   if (a.short_max && G != 1) {
     // hybrid: short segments one lane each, then the rest with G lanes
@@ -530,20 +544,25 @@ cudaError_t launch_segmented(const SegArgs &a, const DevInfo &di, cudaStream_t s
   if (G == 1) {  // one lane per segment
     const unsigned long long need = (a.nseg + kLaneThreads - 1) / kLaneThreads;
     const unsigned g = grid_for(need, (unsigned long long)di.num_sms * di.lane_blocks_per_sm);
-    if (a.seg_off)
+    if (a.seg_off && a.short_max)
+      pp_seglane_kernel<false, true><<<g, kLaneThreads, 0, st>>>(a);
+    else if (a.seg_off)
       pp_seglane_kernel<false><<<g, kLaneThreads, 0, st>>>(a);
     else
       pp_seglane_kernel<true><<<g, kLaneThreads, 0, st>>>(a);
     return cudaGetLastError();
   }
-  unsigned ipc = 0;
   if (seg_use_tma(a, di, &ipc)) {
     const unsigned long long chunks =
         (a.nseg + (unsigned long long)ipc * (32 / G) - 1) / ((unsigned long long)ipc * (32 / G));
     const unsigned g = grid_for(chunks, (unsigned long long)di.num_sms);
     SegArgs b = a;  // dynamic chunk order once CTAs stream tens of chunks
     b.sched = chunks >= 16ull * g ? sched_slot(di, st) : nullptr;
-    if (G == 8)
+    if (G == 2)
+      pp_segtma_kernel<2><<<g, kSegTmaThreads, kSegTmaSmem, st>>>(b, ipc);
+    else if (G == 4)
+      pp_segtma_kernel<4><<<g, kSegTmaThreads, kSegTmaSmem, st>>>(b, ipc);
+    else if (G == 8)
       pp_segtma_kernel<8><<<g, kSegTmaThreads, kSegTmaSmem, st>>>(b, ipc);
     else if (G == 16)
       pp_segtma_kernel<16><<<g, kSegTmaThreads, kSegTmaSmem, st>>>(b, ipc);
@@ -556,12 +575,20 @@ cudaError_t launch_segmented(const SegArgs &a, const DevInfo &di, cudaStream_t s
   const unsigned g = grid_for(need, (unsigned long long)di.num_sms * di.seg_blocks_per_sm);
   SegArgs b = a;  // dynamic group order once warps see several groups each
   b.sched = need >= 4ull * g ? sched_slot(di, st) : nullptr;
-  if (G == 8)
+  if (b.short_max) {
+    if (G == 8)
+      pp_seg_kernel<8, true><<<g, kSegThreads, 0, st>>>(b);
+    else if (G == 16)
+      pp_seg_kernel<16, true><<<g, kSegThreads, 0, st>>>(b);
+    else
+      pp_seg_kernel<32, true><<<g, kSegThreads, 0, st>>>(b);
+  } else if (G == 8) {
     pp_seg_kernel<8><<<g, kSegThreads, 0, st>>>(b);
-  else if (G == 16)
+  } else if (G == 16) {
     pp_seg_kernel<16><<<g, kSegThreads, 0, st>>>(b);
-  else
+  } else {
     pp_seg_kernel<32><<<g, kSegThreads, 0, st>>>(b);
+  }
   return cudaGetLastError();
 }
 

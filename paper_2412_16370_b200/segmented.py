@@ -16,8 +16,11 @@ from . import _lib
 from .core import InputLengthError, InputView, check_width, is_torch_tensor
 
 # arrays up to this many bytes are counted one lane each (pp_seglane_kernel);
-# the C ABI applies the same bound to fixed-size segments
+# when every array starts and ends on a 16-byte boundary the G-lane kernels
+# win above LANE_MAX_ALIGNED (no partial vectors).  The C ABI applies the same
+# bounds to fixed-size segments (scripts/seg_smallG.py).
 LANE_MAX_BYTES = 1024
+LANE_MAX_ALIGNED = 512
 
 
 def _device_view(data):
@@ -76,8 +79,9 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
             if bool((d % step != 0).any()):
                 raise InputLengthError(f"a segment is not a multiple of the {step}-byte word size")
             if lanes is None:  # validation already synchronised: pick the shape too
-                nlong = int((d > LANE_MAX_BYTES).sum())
-                shape = _shape(int(d.numel()), nlong, int(offs[-1] - offs[0]) // d.numel())
+                base_al = (view.base.data_ptr() + view.offset) % 16 == 0
+                shape = _shape(int(d.numel()), int(d.max()), int(offs[-1] - offs[0]) // d.numel(),
+                               base_al and not bool((offs % 16 != 0).any()))
     else:
         offs_np = np.asarray(offsets, dtype=np.int64)
         if offs_np.ndim != 1 or offs_np.size < 1:
@@ -91,8 +95,10 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
         offs = torch.as_tensor(offs_np, device=dev)
         if lanes is None and offs_np.size > 1:
             d = np.diff(offs_np)
-            nlong = int((d > LANE_MAX_BYTES).sum())
-            shape = _shape(int(d.size), nlong, (int(offs_np[-1]) - int(offs_np[0])) // d.size)
+            base_al = (view.base.data_ptr() + view.offset) % 16 == 0
+            shape = _shape(int(d.size), int(d.max()),
+                           (int(offs_np[-1]) - int(offs_np[0])) // d.size,
+                           base_al and not (offs_np % 16).any())
     nseg = offs.numel() - 1
     out, fresh = _out_tensor(out, max(nseg, 0), width, dev)
     if nseg <= 0:
@@ -114,15 +120,16 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
     return out
 
 
-def _shape(nseg, nlong, mean):
+def _shape(nseg, dmax, mean, vec_aligned):
     """Launch shape from the length distribution: (lanes, hybrid).
 
-    Every array <= LANE_MAX_BYTES: one lane each, else G lanes by the mean
-    length.  The hybrid split (PP_SEG_HYBRID, short arrays one lane each in a
-    separate pass) is opt-in: measured, it wins only for strongly bimodal
-    lengths (profiles/r1_segmented_ablation.md).
+    Every array <= LANE_MAX_BYTES (LANE_MAX_ALIGNED when all arrays are
+    16-byte aligned): one lane each, else G lanes by the mean length.  The
+    hybrid split (PP_SEG_HYBRID, short arrays one lane each in a separate
+    pass) is opt-in: measured, it wins only for strongly bimodal lengths
+    (profiles/r1_segmented_ablation.md).
     """
-    if nlong == 0:
+    if dmax <= (LANE_MAX_ALIGNED if vec_aligned else LANE_MAX_BYTES):
         return 1, False
     return (32 if mean >= 16384 else 16 if mean >= 8192 else 8), False
 
@@ -130,8 +137,8 @@ def _shape(nseg, nlong, mean):
 def _lanes_flag(lanes):
     if lanes is None:
         return 0
-    if lanes not in (1, 8, 16, 32):
-        raise ValueError("lanes must be 1, 8, 16 or 32")
+    if lanes not in (1, 2, 4, 8, 16, 32):
+        raise ValueError("lanes must be 1, 2, 4, 8, 16 or 32")
     return lanes << 8
 
 
