@@ -352,8 +352,12 @@ def main_gpu(args):
     peers = None
     if fused:
         from paper_2412_16370_b200.dist import PeerCounters
-        peers = PeerCounters(device=dev)
-        ntgt = len(peers.targets)
+        try:
+            peers = PeerCounters(device=dev)
+            ntgt = len(peers.targets)
+        except RuntimeError as exc:  # no peer access between these GPUs: NCCL exchange
+            print(f"bench: {exc}; using the NCCL exchange", file=sys.stderr)
+            fused, peers = False, None
     globs = [torch.zeros(64, dtype=torch.int64, device=dev) for _ in range(2)]
     count_ev = [torch.cuda.Event() for _ in range(2)]
     snap_ev = [torch.cuda.Event() for _ in range(2)]

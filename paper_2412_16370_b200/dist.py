@@ -73,16 +73,29 @@ class PeerCounters:
             dist.all_gather_object(handles, handle.raw, group=group)
         self._opened = []
         ptrs = []
+        err = None
         with torch.cuda.device(self.device):
-            for r, h in enumerate(handles):
-                if r == self.rank:
-                    ptrs.append(self.local.data_ptr())
-                    continue
-                p = ctypes.c_void_p()
-                _lib.check(self.lib.pp_ipc_open(ctypes.create_string_buffer(h, len(h)),
-                                                ctypes.byref(p)))
-                self._opened.append(p.value)
-                ptrs.append(p.value)
+            try:
+                for r, h in enumerate(handles):
+                    if r == self.rank:
+                        ptrs.append(self.local.data_ptr())
+                        continue
+                    p = ctypes.c_void_p()
+                    _lib.check(self.lib.pp_ipc_open(ctypes.create_string_buffer(h, len(h)),
+                                                    ctypes.byref(p)))
+                    self._opened.append(p.value)
+                    ptrs.append(p.value)
+            except Exception as exc:  # noqa: BLE001 - agreed on below, then raised
+                err = exc
+        if self.world > 1:
+            # every rank must take the same path: agree on success first
+            flag = torch.tensor([0 if err else 1], dtype=torch.int64, device=self.device)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+            if int(flag.item()) == 0 and err is None:
+                err = RuntimeError("a peer rank could not map the counter arrays")
+        if err is not None:
+            self.close()
+            raise RuntimeError(f"fused exchange unavailable (no peer mapping): {err}") from err
         # own array first: it is the kernel's primary target
         ptrs.insert(0, ptrs.pop(self.rank))
         self.targets = (ctypes.c_void_p * len(ptrs))(*ptrs)
