@@ -387,7 +387,7 @@ def main_gpu(args):
                                                    counters2[b].data_ptr(), sp))
             else:
                 _lib.check(lib.pp_count(view_ptr, nbytes, w, counters2[b].data_ptr(), sp))
-        if use_dist:
+        if use_dist and seg_out is None:  # segmented rows stay on their rank
             count_ev[b].record(st)
             side.wait_event(count_ev[b])
             with torch.cuda.stream(side):
@@ -399,7 +399,7 @@ def main_gpu(args):
         nstep[0] += 1
 
     def drain():
-        if use_dist and not fused:  # the last exchanges complete inside the timed region
+        if use_dist and not fused and seg_out is None:  # last exchanges inside the region
             st.wait_event(red_ev[0])
             st.wait_event(red_ev[1])
 
