@@ -642,6 +642,8 @@ def main_gpu(args):
                        "parallelism": (f"dp{world} (shards; fused exchange: the counting "
                                        "kernel adds into every rank's IPC-mapped counters)"
                                        if fused else
+                                       f"dp{world} (segment ranges; rows stay on their rank, "
+                                       "no exchange)" if seg_out is not None else
                                        f"dp{world} (shards, NCCL allreduce of {w} counters "
                                        "per step)") if world > 1 else "single GPU",
                        "l2": "input >> 126 MB L2, no flush needed" if nbytes > 256 * MIB
