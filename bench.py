@@ -238,22 +238,33 @@ def run_reference(args):
     if cfg == "c4seg":
         kind, w, nbytes = "bernoulli", 64, GIB
     nbytes = min(nbytes, GIB)  # bounded sample of the workload (the metric is a rate)
+    unit_bytes = 1  # bytes of the metric's unit per byte counted
     if kind == "uniform":
         host = O.gen_uniform(nbytes, 0xC2 if cfg == "c2" else 0xC1)
     elif kind == "onehot32":
         host = O.gen_onehot32(nbytes, 0xC3)
+    elif kind == "codes8":
+        # the reference counts categories as one-hot words:
+        # 4 bytes of one-hot u32 per code; the metric is per code byte
+        host = O.gen_onehot32(nbytes, 0xC3)
+        unit_bytes = 4
     elif kind == "bernoulli":
         host = O.gen_bernoulli(nbytes, 0xC4, 655)
     else:
         host = O.gen_blocks(nbytes, 0xC5)
     threads = host_threads()
+    if cfg == "c4seg":  # the same 4 KiB segments, one counter row each
+        offs = np.arange(host.size // 4096 + 1, dtype=np.uint64) * 4096
+        run = lambda: O.segments(host, offs, 64, threads=threads)  # noqa: E731
+    else:
+        run = lambda: O.hs512(host, 0, host.size, w, threads=threads)  # noqa: E731
     for _ in range(args.warmup):
-        O.hs512(host, 0, host.size, w, threads=threads)
+        run()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        O.hs512(host, 0, host.size, w, threads=threads)
+        run()
     t = time.perf_counter() - t0
-    value = host.size * args.steps / t / 1e9
+    value = host.size / unit_bytes * args.steps / t / 1e9
     line = {
         "impl": "reference",
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
@@ -264,9 +275,10 @@ def run_reference(args):
         "config": {"workload": desc, "word_width": w, "bytes_per_step": int(host.size)},
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads,
                          "kind": "port",
-                         "sample": f"whole {host.size >> 20} MiB {cfg} array per step; C "
-                                   "restatement of NumbaKernel.run (kernels.py:242-270) on "
-                                   f"{threads} threads over contiguous shards"},
+                         "sample": f"whole {host.size >> 20} MiB {cfg} array per step"
+                                   + (" (one-hot u32 words of the codes)" if unit_bytes == 4
+                                      else "") + "; C restatement of NumbaKernel.run "
+                                   f"(kernels.py:242-270) on {threads} threads"},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
