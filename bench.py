@@ -205,19 +205,26 @@ def host_threads():
 
 # ------------------------------------------------------------ CPU legs
 
-def time_cpu_port(host_u8, w, min_time):
+def time_cpu_port(host_u8, w, min_time, seg=0):
     """Reference harness methodology (bench.py:124-160): k doubles until a
     round lasts >= min_time, >= 2 rounds, report the last.  Returns
-    (GB/s, threads, counters of one pass, k, seconds)."""
+    (GB/s, threads, counters of one pass, k, seconds).  seg > 0: the same
+    bytes as seg-byte segments, one counter row each (the segmented config)."""
+    import numpy as np
     from oracle import oracle as O
     n = host_u8.size
     threads = host_threads()
-    once = O.hs512(host_u8, 0, n, w, threads=threads)  # warm + result
+    if seg:
+        offs = np.arange(n // seg + 1, dtype=np.uint64) * seg
+        one = lambda: O.segments(host_u8, offs, w, threads=threads)  # noqa: E731
+    else:
+        one = lambda: O.hs512(host_u8, 0, n, w, threads=threads)  # noqa: E731
+    once = one()  # warm + result
     k, rounds = 1, 0
     while True:
         t0 = time.perf_counter()
         for _ in range(k):
-            O.hs512(host_u8, 0, n, w, threads=threads)
+            one()
         t = time.perf_counter() - t0
         rounds += 1
         if rounds >= 2 and t >= min_time:
@@ -630,15 +637,26 @@ def main_gpu(args):
         del pinned, res
 
     cpu = None
-    if args.cpu_baseline and world == 1 and rank == 0 and seg_out is None and not categorical:
+    if args.cpu_baseline and world == 1 and rank == 0:
         sample = min(nbytes, 256 * MIB)
-        host = buf[offset:offset + sample].cpu().numpy()
-        gbs, threads, _, k, t = time_cpu_port(host, w, args.cpu_min_time)
+        if categorical:
+            # the reference counts categories as one-hot u32 words: the same
+            # draws materialised (4 bytes per code), reported per code byte
+            from oracle import oracle as O
+            host = O.gen_onehot32(4 * sample, 0xC3)
+            gbs, threads, _, k, t = time_cpu_port(host, 32, args.cpu_min_time)
+            gbs /= 4
+            what = f"the one-hot u32 words of the first {sample >> 20} Mi codes"
+        else:
+            host = buf[offset:offset + sample].cpu().numpy()
+            gbs, threads, _, k, t = time_cpu_port(host, w, args.cpu_min_time,
+                                                  seg=4096 if seg_out is not None else 0)
+            what = (f"first {sample >> 20} MiB of the same {cfg} array"
+                    + (" as 4 KiB segments" if seg_out is not None else ""))
         cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-               "sample": f"first {sample >> 20} MiB of the same {cfg} array, counted {k}x "
-                         f"in {t:.1f} s (last of >=2 rounds); C restatement of "
-                         "NumbaKernel.run (kernels.py:242-270), contiguous shards on "
-                         f"{threads} host threads"}
+               "sample": f"{what}, counted {k}x in {t:.1f} s (last of >=2 rounds); C "
+                         "restatement of NumbaKernel.run (kernels.py:242-270), contiguous "
+                         f"shards on {threads} host threads"}
 
     if rank == 0:
         line = {
