@@ -36,7 +36,10 @@ namespace pp {
 #endif
 constexpr int kTmaConsumerWarps = 8;
 constexpr int kSchedSlotsAlloc = 256;  // = kSchedSlots (scheduler slots per device)
-constexpr int kTmaStages = 3;  // 3 x 32 KiB: best of the scripts/bw_probe.cu sweep (profiles/)
+#ifndef PP_TMA_STAGES
+#define PP_TMA_STAGES 3
+#endif
+constexpr int kTmaStages = PP_TMA_STAGES;  // 3 x 32 KiB: best of the scripts/bw_probe.cu sweep (profiles/)
 constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
 constexpr int kTmaStageVecs = kTmaConsumerWarps * 32 * 8;  // 2048 x 16 B = 32 KiB
 constexpr unsigned long long kTmaStageBytes = kTmaStageVecs * 16ull;
@@ -50,7 +53,10 @@ struct TmaShape {
   static constexpr int kThreads = (NCW + 1) * 32;
   static constexpr int kStageVecs = NCW * 32 * 8;
   static constexpr unsigned long long kStageBytes = kStageVecs * 16ull;
-  static constexpr size_t kSmem = kTmaStages * kStageBytes + 2 * kTmaStages * 8;
+  // ring depth: the counting kernel's is tunable (A/B), the fused producer's
+  // 64 KiB stages allow three
+  static constexpr int kStages = NCW == kTmaConsumerWarps ? kTmaStages : 3;
+  static constexpr size_t kSmem = kStages * kStageBytes + 2 * kStages * 8;
 };
 #ifndef PP_CAT_NCW
 #define PP_CAT_NCW 16
@@ -398,15 +404,15 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   using Sh = TmaShape<NCW>;
   extern __shared__ __align__(128) uint8_t smem[];
   uint4 *stages = reinterpret_cast<uint4 *>(smem);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + kTmaStages * Sh::kStageBytes);
-  uint64_t *empty = full + kTmaStages;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + Sh::kStages * Sh::kStageBytes);
+  uint64_t *empty = full + Sh::kStages;
   __shared__ unsigned long long frame[64];
-  __shared__ unsigned long long chunk_id[kTmaStages];  // written before the stage's arrival
+  __shared__ unsigned long long chunk_id[Sh::kStages];  // written before the stage's arrival
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     PP_TL(0);
-    for (int s = 0; s < kTmaStages; ++s) {
+    for (int s = 0; s < Sh::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NCW);
     }
@@ -444,7 +450,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         mbar_arrive_expect_tx(&full[stage], bytes);
         bulk_g2s(stages + stage * Sh::kStageVecs, a.body + off, bytes, &full[stage], pol);
         ch = a.sched ? gridDim.x + (unsigned long long)atomicAdd(a.sched, 1u) : ch + gridDim.x;
-        if (++stage == kTmaStages) {
+        if (++stage == Sh::kStages) {
           stage = 0;
           phase ^= 1;
         }
@@ -503,7 +509,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
 #pragma unroll
         for (int i = 0; i < 8; ++i) xs ^= v[i].x ^ v[i].y ^ v[i].z ^ v[i].w;
       }
-      if (++stage == kTmaStages) {
+      if (++stage == Sh::kStages) {
         stage = 0;
         phase ^= 1;
       }
