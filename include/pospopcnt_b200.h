@@ -118,7 +118,20 @@ PP_API int pp_count_segmented(const void *base, const unsigned long long *seg_of
                        size_t nseg, int width, unsigned long long *out,
                        int flags, void *stream);
 
-/* pp_count_fixed — as above for nseg equal segments of seg_bytes each. */
+/*
+ * pp_count_batch — many independent arrays at arbitrary device addresses in
+ * one launch: row i of out (DEVICE, n*width uint64, row-major) receives the
+ * count of bytes [ptrs[i], ptrs[i] + lens[i]).  ptrs / lens are DEVICE
+ * arrays of n u64 (absolute addresses, byte lengths; every length a multiple
+ * of width/8, caller-validated).  flags as for pp_count_segmented (default
+ * shape: one warp per array; PP_SEG_LANES(1) one lane each for tiny arrays).
+ * Replaces: n calls of Kernel.run (kernels.py:242), one per array.
+ */
+PP_API int pp_count_batch(const unsigned long long *ptrs, const unsigned long long *lens,
+                          size_t n, int width, unsigned long long *out, int flags,
+                          void *stream);
+
+/* pp_count_fixed — as pp_count_segmented for nseg equal segments of seg_bytes each. */
 PP_API int pp_count_fixed(const void *base, size_t seg_bytes, size_t nseg, int width,
                    unsigned long long *out, int flags, void *stream);
 

@@ -338,6 +338,31 @@ int pp_count_segmented(const void *base, const unsigned long long *seg_off, size
   return seg_common(a, stream);
 }
 
+int pp_count_batch(const unsigned long long *ptrs, const unsigned long long *lens, size_t n,
+                   int width, unsigned long long *out, int flags, void *stream) {
+  if (!width_ok(width)) return fail(PP_EWIDTH, "word width must be one of (8, 16, 32, 64), got %d", width);
+  if (n == 0) return PP_OK;
+  if (!ptrs || !lens) return fail(PP_EARG, "ptrs / lens is NULL");
+  int rc;
+  if ((rc = check_device_ptr(ptrs, "ptrs"))) return rc;
+  if ((rc = check_device_ptr(lens, "lens"))) return rc;
+  if ((rc = check_device_ptr(out, "out"))) return rc;
+  pp::DevInfo di;
+  if ((rc = current_devinfo(&di))) return rc;
+  pp::SegArgs a{};
+  a.ptrs = ptrs;
+  a.lens = lens;
+  a.nseg = n;
+  a.out = out;
+  a.width = width;
+  a.overwrite = (flags & PP_SEG_OVERWRITE) ? 1 : 0;
+  const int g = seg_lanes(flags, 1ull << 20);  // unknown lengths: one warp each
+  a.lanes_per_segment = (g == 2) ? 1 : (g == 4) ? 8 : g;  // no TMA ring for scattered arrays
+  cudaError_t e = pp::launch_segmented(a, di, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "pp_count_batch launch");
+  return PP_OK;
+}
+
 int pp_count_fixed(const void *base, size_t seg_bytes, size_t nseg, int width,
                    unsigned long long *out, int flags, void *stream) {
   if (width_ok(width) && seg_bytes % (size_t)(width / 8))

@@ -42,6 +42,10 @@ struct SegArgs {
   // hybrid split (0 = off): segments of <= short_max bytes are counted one
   // lane each (pp_seglane_kernel), the longer ones by the G-lane kernel
   unsigned long long short_max;
+  // pointer mode (pp_count_batch): segment s = [ptrs[s], ptrs[s] + lens[s]),
+  // device arrays of absolute addresses and byte lengths; base/seg_off unused
+  const unsigned long long *ptrs;
+  const unsigned long long *lens;
 };
 
 enum class LoadPath : int { kTma = 0, kLdg = 1 };

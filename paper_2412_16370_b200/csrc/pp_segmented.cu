@@ -47,8 +47,13 @@ struct SegGeom {
 
 __device__ __forceinline__ SegGeom seg_geom(const SegArgs &a, unsigned long long s) {
   unsigned long long s0 = 0, s1 = 0;
+  uintptr_t origin = reinterpret_cast<uintptr_t>(a.base);
   if (s < a.nseg) {
-    if (a.seg_off) {
+    if (a.ptrs) {  // pointer mode: absolute address + length
+      origin = 0;
+      s0 = a.ptrs[s];
+      s1 = s0 + a.lens[s];
+    } else if (a.seg_off) {
       s0 = a.seg_off[s];
       s1 = a.seg_off[s + 1];
       if (s1 < s0) s1 = s0;
@@ -58,7 +63,7 @@ __device__ __forceinline__ SegGeom seg_geom(const SegArgs &a, unsigned long long
     }
   }
   SegGeom g;
-  g.p0 = reinterpret_cast<uintptr_t>(a.base) + s0;
+  g.p0 = origin + s0;
   g.e = g.p0 + (s1 - s0);
   g.A = g.p0 & ~(uintptr_t)15;
   g.nvv = (s1 > s0) ? (((g.e + 15) & ~(uintptr_t)15) - g.A) >> 4 : 0;
@@ -234,24 +239,29 @@ __device__ __forceinline__ uint32_t byte_range_mask(int q, int lo, int hi) {
   return m1 & m2;
 }
 
-template <bool FIXED, bool HYBRID = false>
+template <bool FIXED, bool HYBRID = false, bool PTRS = false>
 __global__ void __launch_bounds__(kLaneThreads)
     pp_seglane_kernel(SegArgs a) {
   __shared__ uint32_t frs[kLaneWarps][64 * kLaneStride];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t *fr = frs[warp];
-  const uintptr_t base = reinterpret_cast<uintptr_t>(a.base);
+  const uintptr_t base = PTRS ? 0 : reinterpret_cast<uintptr_t>(a.base);
   // the caller's view: vectors entirely inside it are read whole, the
-  // others byte by byte (nothing outside the view is ever read)
-  const uintptr_t view_lo = base + (FIXED ? 0ull : a.seg_off[0]);
-  const uintptr_t view_hi = base + (FIXED ? a.nseg * a.seg_bytes : a.seg_off[a.nseg]);
+  // others byte by byte (nothing outside the view is ever read); in pointer
+  // mode every array is its own view
+  const uintptr_t view_lo = PTRS ? 0 : base + (FIXED ? 0ull : a.seg_off[0]);
+  const uintptr_t view_hi =
+      PTRS ? 0 : base + (FIXED ? a.nseg * a.seg_bytes : a.seg_off[a.nseg]);
   const unsigned long long nw = (unsigned long long)gridDim.x * kLaneWarps;
   for (unsigned long long s0 = ((unsigned long long)blockIdx.x * kLaneWarps + warp) * 32;
        s0 < a.nseg; s0 += nw * 32) {
     const unsigned long long s = s0 + lane;
     unsigned long long b0 = 0, b1 = 0;
     if (s < a.nseg) {
-      if (FIXED) {
+      if (PTRS) {
+        b0 = a.ptrs[s];
+        b1 = b0 + a.lens[s];
+      } else if (FIXED) {
         b0 = s * a.seg_bytes;
         b1 = b0 + a.seg_bytes;
       } else {
@@ -303,9 +313,10 @@ __global__ void __launch_bounds__(kLaneThreads)
         bl[c] = bh[c] = 0u;
       }
     };
+    const uintptr_t vlo = PTRS ? p0 : view_lo, vhi = PTRS ? e : view_hi;
     for (uintptr_t va = p0 & ~(uintptr_t)15; va < e; va += 16) {
       uint4 v;
-      if (va >= view_lo && va + 16 <= view_hi) {
+      if (va >= vlo && va + 16 <= vhi) {
         v = __ldg(reinterpret_cast<const uint4 *>(va));
         if (va < p0 || va + 16 > e) {  // mask to the segment
           const int lo = va < p0 ? (int)(p0 - va) : 0;
@@ -511,7 +522,8 @@ static bool seg_use_tma(const SegArgs &a, const DevInfo &di, unsigned *items_per
   static const char *path = std::getenv("PP_SEG_PATH");
   if (path && std::strcmp(path, "ldg") == 0) return false;
   const bool force = path && std::strcmp(path, "tma") == 0;
-  if (a.seg_off || a.seg_bytes == 0 || (a.seg_bytes & 15) || ((uintptr_t)a.base & 15)) return false;
+  if (a.ptrs || a.seg_off || a.seg_bytes == 0 || (a.seg_bytes & 15) || ((uintptr_t)a.base & 15))
+    return false;
   const unsigned long long item = (unsigned long long)(32 / a.lanes_per_segment) * a.seg_bytes;
   const unsigned long long k = kSegTmaStageBytes / item;
   if (k < (unsigned long long)kSegTmaTeamWarps) return false;
@@ -544,7 +556,9 @@ cudaError_t launch_segmented(const SegArgs &a0, const DevInfo &di, cudaStream_t 
   if (G == 1) {  // one lane per segment
     const unsigned long long need = (a.nseg + kLaneThreads - 1) / kLaneThreads;
     const unsigned g = grid_for(need, (unsigned long long)di.num_sms * di.lane_blocks_per_sm);
-    if (a.seg_off && a.short_max)
+    if (a.ptrs)
+      pp_seglane_kernel<false, false, true><<<g, kLaneThreads, 0, st>>>(a);
+    else if (a.seg_off && a.short_max)
       pp_seglane_kernel<false, true><<<g, kLaneThreads, 0, st>>>(a);
     else if (a.seg_off)
       pp_seglane_kernel<false><<<g, kLaneThreads, 0, st>>>(a);

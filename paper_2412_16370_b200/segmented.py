@@ -168,3 +168,49 @@ def pospopcnt_fixed(data, seg_bytes, width, out=None, accumulate=True, lanes=Non
         _lib.check(lib.pp_count_fixed(view.base.data_ptr() + view.offset, seg_bytes, nseg,
                                       width, out.data_ptr(), flags, stream))
     return out
+
+
+def pospopcnt_batch(arrays, width, out=None, accumulate=True, lanes=None):
+    """Positional counts of many separate device arrays in one launch.
+
+    ``arrays``: a sequence of CUDA tensors and/or InputViews over CUDA
+    tensors, all on one device, each word-complete.  Row i of the returned
+    (n, width) int64 tensor is ``pospopcnt(arrays[i], width)``.  The launch
+    shape follows the lengths (one lane per array when all are at most
+    LANE_MAX_BYTES, else G lanes by the mean length) unless ``lanes`` forces
+    it.  Asynchronous on the current stream (the pointer/length table is
+    copied to the device once per call).
+    """
+    import torch
+    check_width(width)
+    views = [_device_view(a) for a in arrays]
+    n = len(views)
+    if n == 0:
+        raise ValueError("pospopcnt_batch needs at least one array")
+    dev = views[0].base.device
+    step = width // 8
+    ptrs = np.empty(n, dtype=np.uint64)
+    lens = np.empty(n, dtype=np.uint64)
+    for i, v in enumerate(views):
+        if v.base.device != dev:
+            raise ValueError("all arrays must live on one device")
+        if v.nbytes % step:
+            raise InputLengthError(f"array {i}: {v.nbytes} bytes is not a multiple of the "
+                                   f"{step}-byte word size")
+        ptrs[i] = v.base.data_ptr() + v.offset
+        lens[i] = v.nbytes
+    out, fresh = _out_tensor(out, n, width, dev)
+    if lanes is None:
+        dmax, mean = int(lens.max()), int(lens.sum()) // n
+        aligned = not bool(((ptrs % 16) | (lens % 16)).any())
+        lanes = _shape(n, dmax, mean, aligned)[0]
+    table = torch.from_numpy(np.concatenate([ptrs, lens]).view(np.int64)).to(dev)
+    lib = _lib.load()
+    flags = _lib.PP_SEG_ACCUMULATE if (accumulate and not fresh) else _lib.PP_SEG_OVERWRITE
+    flags |= _lanes_flag(lanes)
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(lib.pp_count_batch(table.data_ptr(), table.data_ptr() + 8 * n, n, width,
+                                      out.data_ptr(), flags, stream))
+        table.record_stream(torch.cuda.current_stream(dev))
+    return out

@@ -3,7 +3,7 @@
 
 Random sizes (0 .. ~300 MiB, so both chunk orders), offsets, widths, entry
 points (device counts, host bytes, list / device counters, segmented, fixed,
-categories, all widths), several streams and host threads at once -- every
+batches of separate arrays, categories, all widths), several streams and host threads at once -- every
 result checked against the oracle.  Runs for --seconds; exits 1 on the first
 mismatch and prints the case.
 
@@ -27,7 +27,8 @@ MIB = 1 << 20
 
 
 def one_case(rng, dev_buf, host, stream):
-    kind = rng.choice(["count", "count", "count_list", "host", "seg", "fixed", "cat", "allw"])
+    kind = rng.choice(["count", "count", "count_list", "host", "seg", "fixed", "cat", "allw",
+                       "batch"])
     w = rng.choice((8, 16, 32, 64))
     step = w // 8
     big = rng.random() < 0.15
@@ -73,6 +74,19 @@ def one_case(rng, dev_buf, host, stream):
                               threads=4)
             return kind, (w, seg, nseg, off, lanes), np.array_equal(
                 out.cpu().numpy().view(np.uint64), want)
+        if kind == "batch":
+            k = rng.randrange(1, 400)
+            spans = []
+            for _ in range(k):
+                ln = rng.choice((0, step, 9 * step, rng.randrange(0, 40000) // step * step))
+                st = rng.randrange(0, host.size - ln + 1)
+                spans.append((st, ln))
+            lanes = rng.choice((None, None, 1, 8, 32))
+            out = pp.pospopcnt_batch([pp.InputView(dev_buf, st, ln) for st, ln in spans], w,
+                                     lanes=lanes)
+            got = out.cpu().numpy().view(np.uint64)
+            ok = all(list(got[i]) == O.hs512(host, st, ln, w) for i, (st, ln) in enumerate(spans))
+            return kind, (w, k, lanes), ok
         if kind == "cat":
             dt = rng.choice((np.uint8, np.int16, np.int32))
             nc = rng.randrange(0, 2 * MIB)

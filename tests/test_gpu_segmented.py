@@ -164,3 +164,31 @@ def test_segment_errors(cuda):
     with pytest.raises(pp.InputLengthError):
         pp.pospopcnt_fixed(buf, 3, 16)
     assert pp.pospopcnt_segmented(buf, [0], 8).shape == (0, 8)
+
+
+@pytest.mark.parametrize("lanes", (None, 1, 8, 32))
+def test_batch_of_separate_arrays(cuda, oracle, rng, lanes):
+    """pospopcnt_batch: arrays in separate allocations (and views at odd
+    offsets inside them), each row == that array's own count; every array is
+    read only within its own bounds (exact-size allocations)."""
+    torch, pp = cuda
+    for w in (8, 16, 64):
+        step = w // 8
+        arrays, hosts = [], []
+        for i in range(600):
+            n = rng.choice((0, step, 3 * step, 17 * step, 200 * step,
+                            rng.randrange(0, 20000) // step * step))
+            off = rng.randrange(0, 16)
+            host = np.frombuffer(rng.randbytes(off + n), np.uint8)
+            t = torch.from_numpy(host.copy()).cuda()  # exactly off + n bytes
+            arrays.append(pp.InputView(t, off, n) if off else t)
+            hosts.append(host[off:])
+        out = pp.pospopcnt_batch(arrays, w, lanes=lanes)
+        got = out.cpu().numpy().view(np.uint64)
+        for i, h in enumerate(hosts):
+            assert list(got[i]) == oracle.scalar(h.tobytes(), w), (w, i)
+        # accumulate into the same rows
+        pp.pospopcnt_batch(arrays, w, out=out, lanes=lanes)
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), 2 * got)
+    with pytest.raises(pp.InputLengthError):
+        pp.pospopcnt_batch([torch.zeros(3, dtype=torch.uint8, device="cuda")], 16)
