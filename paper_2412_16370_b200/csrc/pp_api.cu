@@ -560,6 +560,14 @@ bool host_is_pinned(const void *p) {
   }
   return at.type == cudaMemoryTypeHost;
 }
+bool is_device_memory(const void *p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice;
+}
 // Per-thread small-call context: device scratch + pinned result counters
 // (pp_count_sync), and for small host inputs a 1 MiB pinned staging buffer,
 // a 1 MiB device buffer and a stream, so a small pp_count_host is one
@@ -655,6 +663,8 @@ int pp_count_host(const void *host_data, size_t nbytes, int width,
   if (!host_counters) return fail(PP_EARG, "host_counters is NULL");
   if (nbytes == 0) return PP_OK;
   if (!host_data) return fail(PP_EARG, "host_data is NULL");
+  if (is_device_memory(host_data) || is_device_memory(host_counters))
+    return fail(PP_EARG, "pp_count_host takes host buffers (device memory: use pp_count)");
   int rc;
   pp::DevInfo di;
   if ((rc = current_devinfo(&di))) return rc;

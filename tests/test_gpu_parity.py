@@ -252,6 +252,11 @@ def test_c_abi_rejects_host_pointers(cuda):
     assert b"device" in lib.pp_last_error() or b"CUDA" in lib.pp_last_error()
     rc = lib.pp_count(dc.data_ptr(), 64, 12, dc.data_ptr(), None)
     assert rc == _lib.PP_EWIDTH
+    # and the host entry point rejects device memory (it would memcpy from it)
+    out = np.zeros(64, dtype=np.uint64)
+    dd = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    assert lib.pp_count_host(dd.data_ptr(), 64, 8, out.ctypes.data) == _lib.PP_EARG
+    assert lib.pp_count_host(host.ctypes.data, 64, 8, dc.data_ptr()) == _lib.PP_EARG
 
 
 def test_concurrent_threads_distinct_counters(cuda, rng):
