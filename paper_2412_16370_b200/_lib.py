@@ -72,7 +72,12 @@ def load():
                 _build.build()
             lib = ctypes.CDLL(LIB_PATH)
             for name, (res, args) in SIGNATURES.items():
-                f = getattr(lib, name)
+                try:
+                    f = getattr(lib, name)
+                except AttributeError:
+                    if os.environ.get("PP_LIB_PATH"):
+                        continue  # an older A/B build: only its own entry points
+                    raise
                 f.restype = res
                 f.argtypes = args
             if lib.pp_abi_version() != ABI_VERSION:
