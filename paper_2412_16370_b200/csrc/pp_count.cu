@@ -460,7 +460,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         const uint32_t bytes = (uint32_t)(rem < Sh::kStageBytes ? rem : Sh::kStageBytes);
         mbar_arrive_expect_tx(&full[stage], bytes);
         bulk_g2s(stages + stage * Sh::kStageVecs, a.body + off, bytes, &full[stage], pol);
-        ch = a.sched ? gridDim.x + (unsigned long long)atomicAdd(a.sched, 1u) : ch + gridDim.x;
+        ch = a.sched ? gridDim.x + (unsigned long long)(atomicAdd(a.sched, 1u) - a.sched_base)
+                     : ch + gridDim.x;
         if (++stage == Sh::kStages) {
           stage = 0;
           phase ^= 1;
@@ -546,8 +547,6 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   if (threadIdx.x == 0) PP_TL(5);
   if (kCount) fold_frame_to_counters(frame, a);
   if (threadIdx.x == 0) PP_TL(6);
-  // every producer of the grid has drawn its last ticket before its CTA got here
-  if (a.sched && threadIdx.x == 0) sched_rearm(a.sched);
 }
 
 __global__ void __launch_bounds__(kLdgThreads)
@@ -641,7 +640,7 @@ static cudaError_t compute_device_info(int dev, DevInfo *out) {
     d.count_sms = (reserve > 0 && reserve < d.num_sms) ? d.num_sms - reserve : d.num_sms;
   }
   {  // dynamic scheduler slots (sched_slot), zeroed once
-    const size_t bytes = 2 * kSchedSlotsAlloc * sizeof(unsigned int);
+    const size_t bytes = kSchedSlotsAlloc * sizeof(unsigned int);
     if ((e = cudaMalloc(&d.sched, bytes))) return e;
     if ((e = cudaMemset(d.sched, 0, bytes))) return e;
   }
@@ -699,7 +698,13 @@ static unsigned long long pdl_max_body() {
 // PP_STATIC_SCHED=1 forces the static order (A/B runs).
 constexpr int kSchedSlots = kSchedSlotsAlloc;
 constexpr unsigned long long kDynMinChunks = 4096;  // 128 MiB of 32 KiB chunks
-unsigned int *sched_slot(const DevInfo &di, cudaStream_t st) {
+std::unique_lock<std::mutex> sched_lock() {
+  static std::mutex m;
+  return std::unique_lock<std::mutex>(m);
+}
+
+unsigned int *sched_slot(const DevInfo &di, cudaStream_t st, unsigned long long units,
+                         unsigned int *base) {
   static const bool off = std::getenv("PP_STATIC_SCHED") != nullptr;
   if (off || !di.sched) return nullptr;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -709,17 +714,22 @@ unsigned int *sched_slot(const DevInfo &di, cudaStream_t st) {
     cudaGetLastError();
     return nullptr;
   }
-  static std::mutex m;
-  static std::map<std::pair<unsigned int *, unsigned long long>, int> slots;
+  struct Slot {
+    int idx;
+    unsigned int next;  // the counter's value once every launch so far is done
+  };
+  static std::map<std::pair<unsigned int *, unsigned long long>, Slot> slots;
   static std::map<unsigned int *, int> used;
-  std::lock_guard<std::mutex> lk(m);
   const auto key = std::make_pair(di.sched, id);
-  const auto it = slots.find(key);
-  if (it != slots.end()) return di.sched + 2 * it->second;
-  int &n = used[di.sched];
-  if (n >= kSchedSlots) return nullptr;
-  slots[key] = n;
-  return di.sched + 2 * (n++);
+  auto it = slots.find(key);
+  if (it == slots.end()) {
+    int &n = used[di.sched];
+    if (n >= kSchedSlots) return nullptr;
+    it = slots.emplace(key, Slot{n++, 0u}).first;
+  }
+  *base = it->second.next;
+  it->second.next += (unsigned int)units;  // mod 2^32, as on the device
+  return di.sched + it->second.idx;
 }
 
 template <typename Kern>
@@ -731,8 +741,14 @@ static cudaError_t launch_tma(Kern kernel, unsigned grid, unsigned block, size_t
   CountArgs a = a0;
   // the dynamic order pays off once a CTA streams tens of chunks (+6 % at
   // 256 MiB, +2 % at 1 GiB); below that the static order has no tail to
-  // even out and saves the slot lookup (scripts/pdl_sweep.py)
-  a.sched = a.nchunks >= kDynMinChunks ? sched_slot(di, st) : nullptr;
+  // even out and saves the slot lookup (scripts/pdl_sweep.py).  The slot's
+  // base and the launch are one critical section: launches on a stream must
+  // reach it in the order their bases were handed out.
+  std::unique_lock<std::mutex> lk;
+  if (a.nchunks >= kDynMinChunks) {
+    lk = sched_lock();
+    a.sched = sched_slot(di, st, a.nchunks, &a.sched_base);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);

@@ -339,17 +339,6 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
   return r;
 }
 
-// ---- dynamic chunk scheduler (per-stream slot {next ticket, CTAs done}) ----
-// Called by thread 0 of every CTA after the whole CTA is done drawing
-// tickets: the last CTA of the grid re-arms the slot for the next launch on
-// the stream (stream order, or griddepcontrol.wait under PDL, orders it).
-__device__ __forceinline__ void sched_rearm(unsigned int *sched) {
-  if (atomicAdd(sched + 1, 1u) == gridDim.x - 1) {
-    atomicExch(sched, 0u);
-    atomicExch(sched + 1, 0u);
-  }
-}
-
 // ---- mbarrier / bulk-copy (TMA) primitives --------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

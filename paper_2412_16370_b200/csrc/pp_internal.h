@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 namespace pp {
 
 // Split of one contiguous device byte range into a 16-byte aligned body plus
@@ -24,9 +26,12 @@ struct CountArgs {
   // that receive the same counts as `counters`
   int nextra;
   unsigned long long *extra[15];
-  // dynamic chunk scheduler slot {next ticket, CTAs done} (per stream), or
-  // nullptr for the static grid-stride order (graph capture, slots exhausted)
+  // dynamic chunk scheduler: the stream's ticket counter and its value at
+  // this launch's start (tickets are drawn as sched_base, sched_base + 1, ...
+  // mod 2^32), or nullptr for the static grid-stride order (graph capture,
+  // slots exhausted)
   unsigned int *sched;
+  unsigned int sched_base;
 };
 
 struct SegArgs {
@@ -38,7 +43,8 @@ struct SegArgs {
   int width;
   int overwrite;
   int lanes_per_segment;  // G in {1, 8, 16, 32}
-  unsigned int *sched;    // dynamic chunk scheduler slot (TMA ring kernel), or nullptr
+  unsigned int *sched;    // dynamic scheduler ticket counter, or nullptr
+  unsigned int sched_base;  // its value when this launch starts
   // hybrid split (0 = off): segments of <= short_max bytes are counted one
   // lane each (pp_seglane_kernel), the longer ones by the G-lane kernel
   unsigned long long short_max;
@@ -57,7 +63,7 @@ struct DevInfo {
   int ldg_blocks_per_sm;
   int lane_blocks_per_sm;
   int count_sms;  // SMs the persistent counting grid uses (num_sms - PP_RESERVE_SMS)
-  unsigned int *sched;  // kSchedSlots x {next, done}, zeroed (device memory)
+  unsigned int *sched;  // kSchedSlots ticket counters, zeroed (device memory)
   bool ready;
 };
 
@@ -67,9 +73,16 @@ cudaError_t segmented_setup(DevInfo *d);
 
 // "no chunk": the TMA producers' stop sentinel in a stage's chunk-id slot
 constexpr unsigned long long kNoChunk = ~0ull;
-// Per-stream dynamic scheduler slot {next ticket, CTAs done} on di's device,
-// or nullptr (graph capture, slots exhausted, PP_STATIC_SCHED).
-unsigned int *sched_slot(const DevInfo &di, cudaStream_t st);
+// The stream's dynamic-scheduler ticket counter on di's device, or nullptr
+// (graph capture, slots exhausted, PP_STATIC_SCHED).  *base receives the
+// counter's value at the start of this launch; the launch must draw exactly
+// `units` tickets (one per work unit: every unit is a CTA's or warp's first
+// or the reward of one successful draw, and each CTA/warp draws once more
+// to learn it is done), so the next launch's base is base + units.
+// Caller holds sched_lock() from sched_slot() until the launch is enqueued.
+unsigned int *sched_slot(const DevInfo &di, cudaStream_t st, unsigned long long units,
+                         unsigned int *base);
+std::unique_lock<std::mutex> sched_lock();
 
 inline unsigned grid_for(unsigned long long nchunks, unsigned long long cap) {
   const unsigned long long g = nchunks < cap ? nchunks : cap;

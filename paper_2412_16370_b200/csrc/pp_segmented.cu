@@ -201,15 +201,11 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
     }
     if (a.sched) {
       unsigned long long tk = 0;
-      if (lane == 0) tk = atomicAdd(a.sched, 1u);
+      if (lane == 0) tk = (unsigned int)(atomicAdd(a.sched, 1u) - a.sched_base);
       batch = nw + __shfl_sync(FULL, tk, 0);
     } else {
       batch += nw;
     }
-  }
-  if (a.sched) {
-    __syncthreads();
-    if (threadIdx.x == 0) sched_rearm(a.sched);
   }
 }
 
@@ -440,7 +436,8 @@ __global__ void __launch_bounds__(kSegTmaThreads, 1)
         const uint32_t bytes = (uint32_t)(rem < chunk_bytes ? rem : chunk_bytes);
         mbar_arrive_expect_tx(&full[stage], bytes);
         bulk_g2s(stages + stage * kStageVecs, a.base + off, bytes, &full[stage], pol);
-        ch = a.sched ? gridDim.x + (unsigned long long)atomicAdd(a.sched, 1u) : ch + gridDim.x;
+        ch = a.sched ? gridDim.x + (unsigned long long)(atomicAdd(a.sched, 1u) - a.sched_base)
+                     : ch + gridDim.x;
       }
     }
   } else {
@@ -493,8 +490,6 @@ __global__ void __launch_bounds__(kSegTmaThreads, 1)
     }
   }
   }
-  __syncthreads();
-  if (a.sched && threadIdx.x == 0) sched_rearm(a.sched);
 }
 // ------------------------------------------------------------------ host side
 cudaError_t segmented_setup(DevInfo *d) {
@@ -571,7 +566,11 @@ cudaError_t launch_segmented(const SegArgs &a0, const DevInfo &di, cudaStream_t 
         (a.nseg + (unsigned long long)ipc * (32 / G) - 1) / ((unsigned long long)ipc * (32 / G));
     const unsigned g = grid_for(chunks, (unsigned long long)di.num_sms);
     SegArgs b = a;  // dynamic chunk order once CTAs stream tens of chunks
-    b.sched = chunks >= 16ull * g ? sched_slot(di, st) : nullptr;
+    std::unique_lock<std::mutex> lk;  // base hand-out and launch: one critical section
+    if (chunks >= 16ull * g) {
+      lk = sched_lock();
+      b.sched = sched_slot(di, st, chunks, &b.sched_base);
+    }
     if (G == 2)
       pp_segtma_kernel<2><<<g, kSegTmaThreads, kSegTmaSmem, st>>>(b, ipc);
     else if (G == 4)
@@ -588,7 +587,12 @@ cudaError_t launch_segmented(const SegArgs &a0, const DevInfo &di, cudaStream_t 
   const unsigned long long need = (a.nseg + segs_per_block - 1) / segs_per_block;
   const unsigned g = grid_for(need, (unsigned long long)di.num_sms * di.seg_blocks_per_sm);
   SegArgs b = a;  // dynamic group order once warps see several groups each
-  b.sched = need >= 4ull * g ? sched_slot(di, st) : nullptr;
+  // work units = batches of 8 segments (the kernel's tickets)
+  std::unique_lock<std::mutex> lk;  // base hand-out and launch: one critical section
+  if (need >= 4ull * g) {
+    lk = sched_lock();
+    b.sched = sched_slot(di, st, (a.nseg + 7) / 8, &b.sched_base);
+  }
   if (b.short_max) {
     if (G == 8)
       pp_seg_kernel<8, true><<<g, kSegThreads, 0, st>>>(b);

@@ -389,6 +389,25 @@ def test_dynamic_schedule_boundaries_and_streams(cuda, oracle):
     for i, o in enumerate(outs):
         want = oracle.hs512(host, 8 * i, mib128 + 4096 * i, 16)
         assert [int(x) for x in o.cpu()] == [3 * v for v in want], i
+    # two host threads launching onto ONE stream: each launch's ticket base is
+    # handed out and the launch enqueued in one critical section
+    import threading
+    shared = torch.cuda.Stream()
+    outs2 = [torch.zeros(8, dtype=torch.int64, device="cuda") for _ in range(2)]
+
+    def hammer(i):
+        with torch.cuda.stream(shared):
+            for _ in range(6):
+                pp.pospopcnt(pp.InputView(buf, 0, mib128 + 8 * i), 8, counters=outs2[i])
+
+    ths = [threading.Thread(target=hammer, args=(i,)) for i in range(2)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    torch.cuda.synchronize()
+    for i, o in enumerate(outs2):
+        assert [int(x) for x in o.cpu()] == [6 * v for v in oracle.hs512(host, 0, mib128 + 8 * i, 8)]
     # graph capture of a large count: replays stay exact
     c = torch.zeros(32, dtype=torch.int64, device="cuda")
     g = torch.cuda.CUDAGraph()
