@@ -698,6 +698,11 @@ static unsigned long long pdl_max_body() {
 // PP_STATIC_SCHED=1 forces the static order (A/B runs).
 constexpr int kSchedSlots = kSchedSlotsAlloc;
 constexpr unsigned long long kDynMinChunks = 4096;  // 128 MiB of 32 KiB chunks
+static unsigned int *&last_slot_next() {  // guarded by sched_lock()
+  static unsigned int *p = nullptr;
+  return p;
+}
+
 std::unique_lock<std::mutex> sched_lock() {
   static std::mutex m;
   return std::unique_lock<std::mutex>(m);
@@ -729,7 +734,14 @@ unsigned int *sched_slot(const DevInfo &di, cudaStream_t st, unsigned long long 
   }
   *base = it->second.next;
   it->second.next += (unsigned int)units;  // mod 2^32, as on the device
+  last_slot_next() = &it->second.next;
   return di.sched + it->second.idx;
+}
+
+// A launch that failed to enqueue draws no tickets: give its units back
+// (caller still holds sched_lock(), so this is the slot just handed out).
+void sched_rollback(unsigned long long units) {
+  if (last_slot_next()) *last_slot_next() -= (unsigned int)units;
 }
 
 template <typename Kern>
@@ -759,7 +771,9 @@ static cudaError_t launch_tma(Kern kernel, unsigned grid, unsigned block, size_t
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kernel, a, sink);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, a, sink);
+  if (e != cudaSuccess && a.sched) sched_rollback(a.nchunks);
+  return e;
 }
 
 cudaError_t launch_count(const CountArgs &a, LoadPath path, const DevInfo &di,

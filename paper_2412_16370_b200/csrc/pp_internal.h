@@ -83,6 +83,8 @@ constexpr unsigned long long kNoChunk = ~0ull;
 unsigned int *sched_slot(const DevInfo &di, cudaStream_t st, unsigned long long units,
                          unsigned int *base);
 std::unique_lock<std::mutex> sched_lock();
+// undo the last sched_slot() hand-out (its launch failed to enqueue)
+void sched_rollback(unsigned long long units);
 
 inline unsigned grid_for(unsigned long long nchunks, unsigned long long cap) {
   const unsigned long long g = nchunks < cap ? nchunks : cap;

@@ -581,7 +581,9 @@ cudaError_t launch_segmented(const SegArgs &a0, const DevInfo &di, cudaStream_t 
       pp_segtma_kernel<16><<<g, kSegTmaThreads, kSegTmaSmem, st>>>(b, ipc);
     else
       pp_segtma_kernel<32><<<g, kSegTmaThreads, kSegTmaSmem, st>>>(b, ipc);
-    return cudaGetLastError();
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess && b.sched) sched_rollback(chunks);
+    return e;
   }
   const unsigned long long segs_per_block = (kSegThreads / 32) * (32 / G);
   const unsigned long long need = (a.nseg + segs_per_block - 1) / segs_per_block;
@@ -607,7 +609,9 @@ cudaError_t launch_segmented(const SegArgs &a0, const DevInfo &di, cudaStream_t 
   } else {
     pp_seg_kernel<32><<<g, kSegThreads, 0, st>>>(b);
   }
-  return cudaGetLastError();
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && b.sched) sched_rollback((a.nseg + 7) / 8);
+  return e;
 }
 
 }  // namespace pp
