@@ -15,6 +15,14 @@
 namespace pp {
 
 constexpr int kSegThreads = 256;
+// groups of S = 32/G segments per scheduler ticket in pp_seg_kernel
+template <int G>
+constexpr unsigned kSegBatchGroups = G == 8 ? 2u : 1u;
+template <int G>
+constexpr unsigned long long seg_batches(unsigned long long nseg) {
+  const unsigned long long per = (unsigned long long)(32 / G) * kSegBatchGroups<G>;
+  return (nseg + per - 1) / per;
+}
 #ifndef PP_SEG_SMEM_COUNTS
 #define PP_SEG_SMEM_COUNTS true
 #endif
@@ -145,11 +153,13 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
   // group gw first, then (a.sched) tickets of the stream's scheduler slot,
   // one per group of S segments (group nw + ticket), else the grid stride:
   // ragged lengths no longer leave a few warps with most of the bytes
-  // work comes in batches of T groups (8 segments): batch gw first, then
-  // (a.sched) one ticket of the stream's scheduler slot per batch (batch
-  // nw + ticket), else the grid stride -- ragged lengths no longer leave a
-  // few warps with most of the bytes, at one atomic per 8 segments
-  constexpr unsigned T = 8 / S;
+  // work comes in batches of T groups: batch gw first, then (a.sched) one
+  // ticket of the stream's counter per batch (batch nw + ticket), else the
+  // grid stride -- ragged lengths no longer leave a few warps with most of
+  // the bytes.  G = 8 (segments < 8 KiB) batches 8 segments per atomic;
+  // longer segments go one group per ticket (a batch of 8 long segments on
+  // one warp starved the others: 1023 x 64 KiB took 117 instead of 21 us)
+  constexpr unsigned T = kSegBatchGroups<G>;
   for (unsigned long long batch = gw;;) {
     if (batch * T * S >= a.nseg) break;
     for (unsigned tg = 0; tg < T; ++tg) {
@@ -589,11 +599,14 @@ cudaError_t launch_segmented(const SegArgs &a0, const DevInfo &di, cudaStream_t 
   const unsigned long long need = (a.nseg + segs_per_block - 1) / segs_per_block;
   const unsigned g = grid_for(need, (unsigned long long)di.num_sms * di.seg_blocks_per_sm);
   SegArgs b = a;  // dynamic group order once warps see several groups each
-  // work units = batches of 8 segments (the kernel's tickets)
+  // work units = the kernel's batches (its tickets)
+  const unsigned long long batches = G == 8    ? seg_batches<8>(a.nseg)
+                                     : G == 16 ? seg_batches<16>(a.nseg)
+                                               : seg_batches<32>(a.nseg);
   std::unique_lock<std::mutex> lk;  // base hand-out and launch: one critical section
   if (need >= 4ull * g) {
     lk = sched_lock();
-    b.sched = sched_slot(di, st, (a.nseg + 7) / 8, &b.sched_base);
+    b.sched = sched_slot(di, st, batches, &b.sched_base);
   }
   if (b.short_max) {
     if (G == 8)
@@ -610,7 +623,7 @@ cudaError_t launch_segmented(const SegArgs &a0, const DevInfo &di, cudaStream_t 
     pp_seg_kernel<32><<<g, kSegThreads, 0, st>>>(b);
   }
   const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess && b.sched) sched_rollback((a.nseg + 7) / 8);
+  if (e != cudaSuccess && b.sched) sched_rollback(batches);
   return e;
 }
 
