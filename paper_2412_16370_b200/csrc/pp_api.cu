@@ -292,11 +292,10 @@ int pp_count_categories(const void *codes, size_t ncodes, int code_bytes, int wi
 // (4 segments per warp, 4x fewer transposes per segment) below 8 KiB.
 // Lanes per segment: the hint (1, 2, 4, 8, 16 or 32), else from the segment
 // length: one lane each for tiny segments (SWAR kernel), else G-lane groups.
-// Crossover (scripts/seg_smallG.py): the one-lane kernel wins up to 512 B,
-// and up to 1 KiB when segments start/end inside 16-byte vectors (the G-lane
-// kernels then assemble partial vectors byte by byte); aligned 1 KiB
-// segments are 1.75x faster with G = 8.
-static constexpr unsigned long long kLaneAutoMaxBytes = 1024;
+// Crossover (scripts/seg_smallG.py): the one-lane kernel wins up to 512 B;
+// at 1 KiB G = 8 is 1.75x faster on aligned segments and even on misaligned
+// ones (whose partial edge vectors are single loads + masks inside the view).
+static constexpr unsigned long long kLaneAutoMaxBytes = 512;
 static constexpr unsigned long long kLaneAutoMaxAligned = 512;
 
 static int seg_lanes(int flags, unsigned long long avg_bytes, bool vec_aligned = false) {

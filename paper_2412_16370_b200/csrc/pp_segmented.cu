@@ -84,6 +84,33 @@ __device__ __forceinline__ bool seg_partial(const SegGeom &g, unsigned long long
   return (k == 0 && g.hp) || (k == g.nvv - 1 && g.tp);
 }
 
+// 0xFF in bytes [lo, hi) of a u32 holding bytes 4q..4q+3 of a vector
+__device__ __forceinline__ uint32_t byte_range_mask(int q, int lo, int hi) {
+  const int a = min(max(lo - 4 * q, 0), 4), b = min(max(4 * q + 4 - hi, 0), 4);
+  uint32_t m1, m2;
+  asm("shl.b32 %0, %1, %2;" : "=r"(m1) : "r"(0xFFFFFFFFu), "r"(8 * a));  // 32 -> 0
+  asm("shr.b32 %0, %1, %2;" : "=r"(m2) : "r"(0xFFFFFFFFu), "r"(8 * b));
+  return m1 & m2;
+}
+
+// A segment's partial head/tail vector: when the whole aligned 16 bytes lie
+// inside the caller's view (they then belong to neighbouring segments),
+// one vector load and a byte mask; else exact-bounds byte loads.
+__device__ __noinline__ uint4 load_edge(uintptr_t va, uintptr_t p0, uintptr_t e,
+                                           uintptr_t view_lo, uintptr_t view_hi) {
+  if (va >= view_lo && va + 16 <= view_hi) {
+    uint4 v = __ldg(reinterpret_cast<const uint4 *>(va));
+    const int lo = va < p0 ? (int)(p0 - va) : 0;
+    const int hi = va + 16 > e ? (int)(e - va) : 16;
+    v.x &= byte_range_mask(0, lo, hi);
+    v.y &= byte_range_mask(1, lo, hi);
+    v.z &= byte_range_mask(2, lo, hi);
+    v.w &= byte_range_mask(3, lo, hi);
+    return v;
+  }
+  return load_partial(va, p0, e);
+}
+
 // Row s of out <- the counts lane r of the segment's G-lane group holds
 // (frame bits G*f + r and 32 + G*f + r), rotated by rot = 8*(p0 mod 8) and
 // folded mod w exactly like flush_fw (accumulate.py:115-130).  All G lanes of
@@ -150,6 +177,11 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
   const unsigned long long gw = (blockIdx.x * (unsigned long long)kSegThreads + threadIdx.x) >> 5;
   const unsigned long long nw = (gridDim.x * (unsigned long long)kSegThreads) >> 5;
   const TC t = make_tc(lane);
+  // the caller's view (pointer mode: none -- every array is its own view)
+  const uintptr_t base_u = reinterpret_cast<uintptr_t>(a.base);
+  const uintptr_t view_lo = a.ptrs ? 0 : base_u + (a.seg_off ? a.seg_off[0] : 0ull);
+  const uintptr_t view_hi =
+      a.ptrs ? 0 : base_u + (a.seg_off ? a.seg_off[a.nseg] : a.nseg * a.seg_bytes);
   // group gw first, then (a.sched) tickets of the stream's scheduler slot,
   // one per group of S segments (group nw + ticket), else the grid stride:
   // ragged lengths no longer leave a few warps with most of the bytes
@@ -192,7 +224,7 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
             if (k < g.nvv) {
               const uintptr_t va = g.A + 16 * k;
               if (seg_partial(g, k))
-                v[j] = load_partial(va, g.p0, g.e);
+                v[j] = load_edge(va, g.p0, g.e, view_lo, view_hi);
               else
                 v[j] = ldg_stream(reinterpret_cast<const uint4 *>(va));
             }
@@ -235,15 +267,6 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
 constexpr int kLaneWarps = 4;
 constexpr int kLaneThreads = kLaneWarps * 32;
 constexpr int kLaneStride = 33;  // fr[pos * 33 + lane]
-
-// 0xFF in bytes [lo, hi) of a u32 holding bytes 4q..4q+3 of a vector
-__device__ __forceinline__ uint32_t byte_range_mask(int q, int lo, int hi) {
-  const int a = min(max(lo - 4 * q, 0), 4), b = min(max(4 * q + 4 - hi, 0), 4);
-  uint32_t m1, m2;
-  asm("shl.b32 %0, %1, %2;" : "=r"(m1) : "r"(0xFFFFFFFFu), "r"(8 * a));  // 32 -> 0
-  asm("shr.b32 %0, %1, %2;" : "=r"(m2) : "r"(0xFFFFFFFFu), "r"(8 * b));
-  return m1 & m2;
-}
 
 template <bool FIXED, bool HYBRID = false, bool PTRS = false>
 __global__ void __launch_bounds__(kLaneThreads)

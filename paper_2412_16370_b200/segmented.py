@@ -19,7 +19,7 @@ from .core import InputLengthError, InputView, check_width, is_torch_tensor
 # when every array starts and ends on a 16-byte boundary the G-lane kernels
 # win above LANE_MAX_ALIGNED (no partial vectors).  The C ABI applies the same
 # bounds to fixed-size segments (scripts/seg_smallG.py).
-LANE_MAX_BYTES = 1024
+LANE_MAX_BYTES = 512
 LANE_MAX_ALIGNED = 512
 
 
