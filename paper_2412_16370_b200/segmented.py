@@ -76,29 +76,26 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
             bad_order = bool((d < 0).any()) or int(offs[0]) < 0 or int(offs[-1]) > view.nbytes
             if bad_order:
                 raise ValueError("offsets must be non-decreasing and inside the view")
-            if bool((d % step != 0).any()):
+            if bool(((d & (step - 1)) != 0).any()):
                 raise InputLengthError(f"a segment is not a multiple of the {step}-byte word size")
             if lanes is None:  # validation already synchronised: pick the shape too
-                base_al = (view.base.data_ptr() + view.offset) % 16 == 0
                 shape = _shape(int(d.numel()), int(d.max()), int(offs[-1] - offs[0]) // d.numel(),
-                               base_al and not bool((offs % 16 != 0).any()))
+                               _aligned_offsets(view, offs))
     else:
         offs_np = np.asarray(offsets, dtype=np.int64)
         if offs_np.ndim != 1 or offs_np.size < 1:
             raise ValueError("offsets must be a 1-D sequence of nseg+1 byte offsets")
+        d = np.diff(offs_np) if (validate or lanes is None) else None
         if validate:
-            d = np.diff(offs_np)
             if (d < 0).any() or offs_np[0] < 0 or offs_np[-1] > view.nbytes:
                 raise ValueError("offsets must be non-decreasing and inside the view")
-            if (d % step).any():
+            if (d & (step - 1)).any():
                 raise InputLengthError(f"a segment is not a multiple of the {step}-byte word size")
         offs = torch.as_tensor(offs_np, device=dev)
         if lanes is None and offs_np.size > 1:
-            d = np.diff(offs_np)
-            base_al = (view.base.data_ptr() + view.offset) % 16 == 0
             shape = _shape(int(d.size), int(d.max()),
                            (int(offs_np[-1]) - int(offs_np[0])) // d.size,
-                           base_al and not (offs_np % 16).any())
+                           _aligned_offsets(view, offs_np))
     nseg = offs.numel() - 1
     out, fresh = _out_tensor(out, max(nseg, 0), width, dev)
     if nseg <= 0:
@@ -132,6 +129,16 @@ def _shape(nseg, dmax, mean, vec_aligned):
     if dmax <= (LANE_MAX_ALIGNED if vec_aligned else LANE_MAX_BYTES):
         return 1, False
     return (32 if mean >= 16384 else 16 if mean >= 8192 else 8), False
+
+
+def _aligned_offsets(view, offs):
+    """Do all segments start on 16-byte boundaries?  Only computed when the
+    shape rule depends on it (LANE_MAX_ALIGNED != LANE_MAX_BYTES)."""
+    if LANE_MAX_ALIGNED == LANE_MAX_BYTES:
+        return False
+    if (view.base.data_ptr() + view.offset) % 16:
+        return False
+    return not bool(((offs & 15) != 0).any())
 
 
 def _lanes_flag(lanes):
@@ -183,22 +190,34 @@ def pospopcnt_batch(arrays, width, out=None, accumulate=True, lanes=None):
     """
     import torch
     check_width(width)
-    views = [_device_view(a) for a in arrays]
-    n = len(views)
+    n = len(arrays)
     if n == 0:
         raise ValueError("pospopcnt_batch needs at least one array")
-    dev = views[0].base.device
     step = width // 8
     ptrs = np.empty(n, dtype=np.uint64)
     lens = np.empty(n, dtype=np.uint64)
-    for i, v in enumerate(views):
-        if v.base.device != dev:
+    dev = None
+    for i, a in enumerate(arrays):
+        if isinstance(a, torch.Tensor):  # fast path: no view object per array
+            if not a.is_cuda:
+                raise ValueError("pospopcnt_batch needs CUDA tensors")
+            if not a.is_contiguous():
+                raise ValueError("input tensor must be contiguous")
+            d, ptr, nb = a.device, a.data_ptr(), a.numel() * a.element_size()
+        else:
+            v = _device_view(a)
+            d, ptr, nb = v.base.device, v.base.data_ptr() + v.offset, v.nbytes
+        if dev is None:
+            dev = d
+        elif d != dev:
             raise ValueError("all arrays must live on one device")
-        if v.nbytes % step:
-            raise InputLengthError(f"array {i}: {v.nbytes} bytes is not a multiple of the "
-                                   f"{step}-byte word size")
-        ptrs[i] = v.base.data_ptr() + v.offset
-        lens[i] = v.nbytes
+        ptrs[i] = ptr
+        lens[i] = nb
+    bad = np.nonzero(lens & np.uint64(step - 1))[0]
+    if bad.size:
+        i = int(bad[0])
+        raise InputLengthError(f"array {i}: {int(lens[i])} bytes is not a multiple of the "
+                               f"{step}-byte word size")
     out, fresh = _out_tensor(out, n, width, dev)
     if lanes is None:
         dmax, mean = int(lens.max()), int(lens.sum()) // n
