@@ -55,10 +55,11 @@ extern "C" {
 /* flags for the segmented entry points */
 #define PP_SEG_ACCUMULATE 0  /* out[s*w+j] += count (reference semantics)  */
 #define PP_SEG_OVERWRITE  1  /* out[s*w+j]  = count (fresh counter rows)   */
-/* optional launch-shape hint: lanes per segment (1, 8, 16 or 32) in bits 8-15;
- * 0 = automatic (fixed: 1 up to 1024-byte segments, else from seg_bytes;
- * CSR: 32 = one warp per segment).  1 = one lane per segment (SWAR counts,
- * for arrays of a few words; a long segment then runs on a single lane). */
+/* optional launch-shape hint: lanes per segment (1, 2, 4, 8, 16 or 32) in bits 8-15;
+ * 0 = automatic (fixed: 1 up to 512-byte segments, else from seg_bytes;
+ * CSR / batch: 8).  1 = one lane per segment (SWAR counts, for arrays of a
+ * few words; a long segment then runs on a single lane); 2 / 4 = the TMA
+ * ring's shapes for 1-2 KiB fixed segments. */
 #define PP_SEG_LANES(g)   ((g) << 8)
 /* CSR only, opt-in: arrays of <= 1024 bytes are counted one lane each and
  * the longer ones with the PP_SEG_LANES shape (two launches, each row written
@@ -124,7 +125,7 @@ PP_API int pp_count_segmented(const void *base, const unsigned long long *seg_of
  * count of bytes [ptrs[i], ptrs[i] + lens[i]).  ptrs / lens are DEVICE
  * arrays of n u64 (absolute addresses, byte lengths; every length a multiple
  * of width/8, caller-validated).  flags as for pp_count_segmented (default
- * shape: one warp per array; PP_SEG_LANES(1) one lane each for tiny arrays).
+ * shape: 8 lanes per array; PP_SEG_LANES(1) one lane each for tiny arrays).
  * Replaces: n calls of Kernel.run (kernels.py:242), one per array.
  */
 PP_API int pp_count_batch(const unsigned long long *ptrs, const unsigned long long *lens,

@@ -59,7 +59,7 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
     lengths (host offsets, or device offsets with ``validate``): one lane per
     segment when every segment is at most LANE_MAX_BYTES, else G lanes by the
     mean length; unknown lengths (device offsets, ``validate=False``) get the
-    C ABI default, G = 32.  ``hybrid=True`` adds a one-lane pass for the
+    C ABI default, G = 8.  ``hybrid=True`` adds a one-lane pass for the
     segments of at most LANE_MAX_BYTES (PP_SEG_HYBRID), which pays for
     strongly bimodal lengths.
     """
