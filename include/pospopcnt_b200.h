@@ -61,7 +61,7 @@ extern "C" {
  * few words; a long segment then runs on a single lane); 2 / 4 = the TMA
  * ring's shapes for 1-2 KiB fixed segments. */
 #define PP_SEG_LANES(g)   ((g) << 8)
-/* CSR only, opt-in: arrays of <= 1024 bytes are counted one lane each and
+/* CSR only, opt-in: arrays of <= 512 bytes are counted one lane each and
  * the longer ones with the PP_SEG_LANES shape (two launches, each row written
  * once).  Pays for strongly bimodal lengths (profiles/r1_segmented_ablation.md). */
 #define PP_SEG_HYBRID     (1 << 16)
