@@ -102,8 +102,15 @@ __device__ __forceinline__ void fold_frame_to_counters(const unsigned long long 
     unsigned long long s = 0;
     for (int i = j; i < 64; i += width) s += frame[(i + a.rot) & 63];
     if (s) {
-      atomicAdd(a.counters + j, s);
-      for (int k = 0; k < a.nextra; ++k) atomicAdd(a.extra[k] + j, s);
+      if (a.nextra == 0) {
+        atomicAdd(a.counters + j, s);
+      } else {
+        // several GPUs add into the same arrays: system scope, so the adds of
+        // different devices are atomic with respect to each other (PTX memory
+        // model; device scope only orders this GPU's threads)
+        atomicAdd_system(a.counters + j, s);
+        for (int k = 0; k < a.nextra; ++k) atomicAdd_system(a.extra[k] + j, s);
+      }
     }
   }
 }
@@ -262,6 +269,45 @@ __device__ __forceinline__ void eat_codes(Counter &c, const uint4 (&v)[8], uint3
       }
       c.eat8(u, t);
     }
+  }
+}
+
+// Fast path for W = 32 when every code of the warp's 8 vectors is < 32 (the
+// caller votes): no range handling, so a code needs no clean byte -- SHF.L.W
+// takes its shift amount mod 32 -- and bytes 1-3 are brought down with
+// IMAD.HI (mul.hi by 2^(32-8k); ptxas keeps it on the FMA pipe) instead of
+// PRMT / SHF on the ALU pipe.  Per 4 codes: 4 SHF on the ALU pipe + 3 IMAD.HI,
+// vs 8 ALU ops in eat_codes.  Measured: ALU pipe 95 -> 79 %, but the kernel
+// is then latency-/dispatch-limited (16 consumer warps): 3889 -> 3982 GB/s
+// (profiles/r1_categories_ablation.md).  The same trick at W = 16 (two codes
+// per word) saves no instructions and its vote costs 3.5 %: not used there.
+#ifndef PP_CAT_SMALL
+#define PP_CAT_SMALL 1
+#endif
+__device__ __forceinline__ uint32_t hi_bytes(uint32_t x, int k) {  // x >> 8k, k = 1..3
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(1u << (32 - 8 * k)));
+  return r;
+}
+__device__ __forceinline__ uint32_t oh_wrap(uint32_t n) {  // 1 << (n mod 32)
+  return __funnelshift_l(0u, 1u, n);
+}
+__device__ __forceinline__ void eat_small_codes32(Counter &c, const uint4 (&v)[8], const TC &t) {
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    uint4 u[8];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const uint4 x = v[2 * h + i];
+      const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t wd = w4[q];
+        u[4 * i + q] = make_uint4(oh_wrap(wd), oh_wrap(hi_bytes(wd, 1)), oh_wrap(hi_bytes(wd, 2)),
+                                  oh_wrap(hi_bytes(wd, 3)));
+      }
+    }
+    c.eat8(u, t);
   }
 }
 
@@ -508,8 +554,19 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
+      // W = 32 u8 codes: vote (whole warp, converged here) for the fast
+      // path -- full chunk and every code < 32
+      bool small = false;
+      if (PP_CAT_SMALL && MODE == 32 && CB == 1) {
+        uint32_t o = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o |= v[i].x | v[i].y | v[i].z | v[i].w;
+        small = __all_sync(FULL, valid == 0xFFu && (o & 0xE0E0E0E0u) == 0u);
+      }
       if (MODE == 1) {
         c.eat8(v, t);
+      } else if (MODE == 32 && CB == 1 && small) {
+        eat_small_codes32(c, v, t);
       } else if (MODE >= 8 && CB == 1) {
         if (valid == 0xFFu)
           eat_codes<(MODE >= 8 ? MODE : 8), true>(c, v, valid, t);

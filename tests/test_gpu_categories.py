@@ -73,6 +73,33 @@ def test_every_u8_code_at_every_byte_position(cuda, oracle):
             assert pp.pospopcnt_categories(codes, w) == oracle.categories(host, w), (w, host.size)
 
 
+@pytest.mark.parametrize("w", (16, 32))
+def test_small_code_fast_path_mixed_with_exact_path(cuda, oracle, w):
+    """w = 32 takes a fast expansion when a warp's 8 vectors hold only codes
+    < 32 (shift amounts taken mod 32, bytes brought down by mul.hi); w = 16
+    runs the same inputs through the exact path.  Every code < w, then the
+    same with one out-of-range code (w, 255, or a value whose low 5 bits
+    alias a valid code) planted in every 7th 4 KiB block, so warps of one
+    launch switch between the two paths; and the partial last chunk."""
+    torch, pp = cuda
+    rng = np.random.default_rng(1000 + w)
+    n = (48 << 20) + 4099
+    host = rng.integers(0, w, n).astype(np.uint8)
+    codes = torch.from_numpy(host).cuda()
+    assert pp.pospopcnt_categories(codes, w) == oracle.categories(host, w)
+    mixed = host.copy()
+    bad = np.array([w, 255, w + 1, 32 + 3, 64 + 5, 128], dtype=np.uint8)
+    pos = np.arange(0, n, 7 * 4096) + rng.integers(0, 4096, (n + 7 * 4096 - 1) // (7 * 4096))
+    pos = pos[pos < n]
+    mixed[pos] = bad[np.arange(pos.size) % bad.size]
+    codes = torch.from_numpy(mixed).cuda()
+    assert pp.pospopcnt_categories(codes, w) == oracle.categories(mixed, w)
+    for m in (1, 15, 16 * 1024 + 3, (1 << 20) - 1):  # short, and partial last chunks
+        assert pp.pospopcnt_categories(codes[:m], w) == oracle.categories(mixed[:m], w), m
+    shifted = torch.from_numpy(np.concatenate([np.zeros(5, np.uint8), host])).cuda()[5:]
+    assert pp.pospopcnt_categories(shifted, w) == oracle.categories(host, w)
+
+
 @pytest.mark.parametrize("dtype", ("int16", "uint16", "int32", "uint32"))
 def test_wide_codes_boundaries_every_lane(cuda, oracle, dtype):
     """2- and 4-byte codes on the one-hot TMA path: boundary values (w - 1,
