@@ -45,6 +45,9 @@ constexpr int kTmaStageVecs = kTmaConsumerWarps * 32 * 8;  // 2048 x 16 B = 32 K
 constexpr unsigned long long kTmaStageBytes = kTmaStageVecs * 16ull;
 constexpr size_t kTmaSmemBytes = kTmaStages * kTmaStageBytes + 2 * kTmaStages * 8;
 
+#ifndef PP_CAT_STAGES
+#define PP_CAT_STAGES 3
+#endif
 // Shape of the TMA pipeline for NCW consumer warps (8 vectors per thread per
 // stage).  The counting kernel uses 8 warps; the fused one-hot producer does
 // ~4x more ALU work per byte and uses more consumer warps.
@@ -55,7 +58,7 @@ struct TmaShape {
   static constexpr unsigned long long kStageBytes = kStageVecs * 16ull;
   // ring depth: the counting kernel's is tunable (A/B), the fused producer's
   // 64 KiB stages allow three
-  static constexpr int kStages = NCW == kTmaConsumerWarps ? kTmaStages : 3;
+  static constexpr int kStages = NCW == kTmaConsumerWarps ? kTmaStages : PP_CAT_STAGES;
   static constexpr size_t kSmem = kStages * kStageBytes + 2 * kStages * 8;
 };
 #ifndef PP_CAT_NCW
@@ -108,6 +111,36 @@ __device__ __forceinline__ void fold_frame_to_counters(const unsigned long long 
         // several GPUs add into the same arrays: system scope, so the adds of
         // different devices are atomic with respect to each other (PTX memory
         // model; device scope only orders this GPU's threads)
+        atomicAdd_system(a.counters + j, s);
+        for (int k = 0; k < a.nextra; ++k) atomicAdd_system(a.extra[k] + j, s);
+      }
+    }
+  }
+}
+
+// The same fold over per-warp frame rows (the TMA kernel): thread j < w sums
+// rows[k][(i + rot) mod 64] over i = j (mod w) and the NCW consumer warps.
+// Replaces 2 x 32 u64 shared atomicAdd per warp -- compiled as CAS loops,
+// with all 8 warps contending for the same 64 words -- by plain stores.
+#ifndef PP_EPI_SLOTS
+#define PP_EPI_SLOTS 1
+#endif
+template <int NCW>
+__device__ __forceinline__ void fold_rows_to_counters(const unsigned long long (*rows)[64],
+                                                      const CountArgs &a) {
+  const int j = threadIdx.x, width = a.width;
+  if (j < width) {
+    unsigned long long s = 0;
+    for (int i = j; i < 64; i += width) {
+      const int p = (i + a.rot) & 63;
+#pragma unroll
+      for (int k = 0; k < NCW; ++k) s += rows[k][p];
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // see fold_frame_to_counters
+    if (s) {
+      if (a.nextra == 0) {
+        atomicAdd(a.counters + j, s);
+      } else {
         atomicAdd_system(a.counters + j, s);
         for (int k = 0; k < a.nextra; ++k) atomicAdd_system(a.extra[k] + j, s);
       }
@@ -463,7 +496,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   uint4 *stages = reinterpret_cast<uint4 *>(smem);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + Sh::kStages * Sh::kStageBytes);
   uint64_t *empty = full + Sh::kStages;
-  __shared__ unsigned long long frame[64];
+  __shared__ unsigned long long frame[PP_EPI_SLOTS ? 1 : 64];
+  __shared__ unsigned long long wframe[PP_EPI_SLOTS ? NCW : 1][64];  // per-warp frame rows
   __shared__ unsigned long long chunk_id[Sh::kStages];  // written before the stage's arrival
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -475,7 +509,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     }
     fence_mbar_init();
   }
-  if (threadIdx.x < 64) frame[threadIdx.x] = 0;
+  if (!PP_EPI_SLOTS && threadIdx.x < 64) frame[threadIdx.x] = 0;
   __syncthreads();
 
   const unsigned long long nchunks = a.nchunks;
@@ -590,8 +624,13 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       if (threadIdx.x == 0) PP_TL(4);
       c.finish(t);
       if (blockIdx.x == 0 && warp == 0) edge_count<kEdgeCB>(c, edge, a.width, t);
-      atomicAdd(&frame[lane], c.ce);
-      atomicAdd(&frame[32 + lane], c.co);
+      if (PP_EPI_SLOTS) {  // one row per warp: plain stores, summed by the fold
+        wframe[warp][lane] = c.ce;
+        wframe[warp][32 + lane] = c.co;
+      } else {  // u64 shared atomics (a CAS loop in SASS, 8 warps contending)
+        atomicAdd(&frame[lane], c.ce);
+        atomicAdd(&frame[32 + lane], c.co);
+      }
     } else {
       xs = __reduce_xor_sync(FULL, xs);
       if (lane == 0) {
@@ -602,7 +641,12 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   }
   __syncthreads();
   if (threadIdx.x == 0) PP_TL(5);
-  if (kCount) fold_frame_to_counters(frame, a);
+  if (kCount) {
+    if (PP_EPI_SLOTS)
+      fold_rows_to_counters<NCW>(wframe, a);
+    else
+      fold_frame_to_counters(frame, a);
+  }
   if (threadIdx.x == 0) PP_TL(6);
 }
 
