@@ -65,6 +65,10 @@ extern "C" {
  * the longer ones with the PP_SEG_LANES shape (two launches, each row written
  * once).  Pays for strongly bimodal lengths (profiles/r1_segmented_ablation.md). */
 #define PP_SEG_HYBRID     (1 << 16)
+/* optional tuning hint for the G-lane kernel: groups of 32/G segments per
+ * dynamic-scheduler ticket, 1-63 in bits 20-25 (0 = automatic: the smallest
+ * batch that keeps a launch under ~49k tickets). */
+#define PP_SEG_BATCH(t)   ((t) << 20)
 
 PP_API int         pp_abi_version(void);
 PP_API const char *pp_strerror(int code);

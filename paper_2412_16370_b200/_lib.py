@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("PP_LIB_PATH") or os.path.join(HERE, "libpospopcnt_b20
 PP_OK, PP_EWIDTH, PP_ELENGTH, PP_ECUDA, PP_EARG, PP_ENODEV = range(6)
 PP_SEG_ACCUMULATE, PP_SEG_OVERWRITE = 0, 1
 PP_SEG_HYBRID = 1 << 16    # CSR: <= 512 B arrays one lane each, the rest G lanes
+PP_SEG_BATCH_SHIFT = 20    # PP_SEG_BATCH(t): groups per scheduler ticket hint (0 = auto)
 PP_MAX_TARGETS = 16        # pp_count_multi: counter arrays per call
 PP_IPC_HANDLE_BYTES = 72   # pp_ipc_handle: CUDA IPC handle + offset in the allocation
 ABI_VERSION = 1

@@ -309,6 +309,9 @@ static int seg_lanes(int flags, unsigned long long avg_bytes, bool vec_aligned =
   return 8;
 }
 
+// PP_SEG_BATCH hint (0 = automatic)
+static unsigned seg_batch_hint(int flags) { return (unsigned)((flags >> 20) & 0x3F); }
+
 static int seg_common(const pp::SegArgs &a, void *stream) {
   if (!width_ok(a.width)) return fail(PP_EWIDTH, "word width must be one of (8, 16, 32, 64), got %d", a.width);
   if (a.nseg == 0) return PP_OK;
@@ -333,6 +336,7 @@ int pp_count_segmented(const void *base, const unsigned long long *seg_off, size
   a.out = out;
   a.width = width;
   a.overwrite = (flags & PP_SEG_OVERWRITE) ? 1 : 0;
+  a.batch_groups = seg_batch_hint(flags);
   // unknown lengths: G = 8 -- within 10 % of G = 32 on long segments and
   // 15-25 % faster on short or skewed ones (scripts/seg_ragged.py)
   a.lanes_per_segment = seg_lanes(flags, kUnknownLengthBytes);
@@ -359,6 +363,7 @@ int pp_count_batch(const unsigned long long *ptrs, const unsigned long long *len
   a.out = out;
   a.width = width;
   a.overwrite = (flags & PP_SEG_OVERWRITE) ? 1 : 0;
+  a.batch_groups = seg_batch_hint(flags);
   const int g = seg_lanes(flags, kUnknownLengthBytes);  // as for CSR offsets
   a.lanes_per_segment = (g == 2) ? 1 : (g == 4) ? 8 : g;  // no TMA ring for scattered arrays
   cudaError_t e = pp::launch_segmented(a, di, static_cast<cudaStream_t>(stream));
@@ -379,6 +384,7 @@ int pp_count_fixed(const void *base, size_t seg_bytes, size_t nseg, int width,
   a.out = out;
   a.width = width;
   a.overwrite = (flags & PP_SEG_OVERWRITE) ? 1 : 0;
+  a.batch_groups = seg_batch_hint(flags);
   a.lanes_per_segment =
       seg_lanes(flags, seg_bytes, ((uintptr_t)base % 16 == 0) && (seg_bytes % 16 == 0));
   return seg_common(a, stream);

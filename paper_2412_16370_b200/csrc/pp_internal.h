@@ -43,6 +43,9 @@ struct SegArgs {
   int width;
   int overwrite;
   int lanes_per_segment;  // G in {1, 8, 16, 32}
+  // pp_seg_kernel: groups of 32/G segments per scheduler ticket (>= 1; 0 =
+  // automatic, resolved by launch_segmented)
+  unsigned int batch_groups;
   unsigned int *sched;    // dynamic scheduler ticket counter, or nullptr
   unsigned int sched_base;  // its value when this launch starts
   // hybrid split (0 = off): segments of <= short_max bytes are counted one

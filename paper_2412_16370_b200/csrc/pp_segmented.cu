@@ -15,12 +15,24 @@
 namespace pp {
 
 constexpr int kSegThreads = 256;
-// groups of S = 32/G segments per scheduler ticket in pp_seg_kernel
-template <int G>
-constexpr unsigned kSegBatchGroups = G == 8 ? 2u : 1u;
-template <int G>
-constexpr unsigned long long seg_batches(unsigned long long nseg) {
-  const unsigned long long per = (unsigned long long)(32 / G) * kSegBatchGroups<G>;
+// Groups of S = 32/G segments per scheduler ticket in pp_seg_kernel.  Every
+// ticket is one atomic on the stream's single counter, and same-address
+// atomics serialise at ~2-3 ns each: 262,144 tickets (1 GiB of 4 KiB
+// segments at G = 32, one segment per ticket) took 592 instead of 200 us.
+// Below ~50k tickets per launch the finest batches balance ragged lengths
+// best (scripts/seg_shape_sweep.py, profiles/r1_segmented_ablation.md), so
+// the batch is the smallest T that keeps the launch under kSegMaxTickets.
+constexpr unsigned long long kSegMaxTickets = 49152;
+constexpr unsigned kSegMaxBatchGroups = 63;
+static unsigned seg_batch_groups(unsigned long long nseg, int G) {
+  const unsigned long long groups = (nseg + (32 / G) - 1) / (32 / G);
+  unsigned long long t = (groups + kSegMaxTickets - 1) / kSegMaxTickets;
+  if (t < 1) t = 1;
+  if (t > kSegMaxBatchGroups) t = kSegMaxBatchGroups;
+  return (unsigned)t;
+}
+static unsigned long long seg_batches(unsigned long long nseg, int G, unsigned T) {
+  const unsigned long long per = (unsigned long long)(32 / G) * T;
   return (nseg + per - 1) / per;
 }
 #ifndef PP_SEG_SMEM_COUNTS
@@ -188,10 +200,11 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
   // work comes in batches of T groups: batch gw first, then (a.sched) one
   // ticket of the stream's counter per batch (batch nw + ticket), else the
   // grid stride -- ragged lengths no longer leave a few warps with most of
-  // the bytes.  G = 8 (segments < 8 KiB) batches 8 segments per atomic;
-  // longer segments go one group per ticket (a batch of 8 long segments on
-  // one warp starved the others: 1023 x 64 KiB took 117 instead of 21 us)
-  constexpr unsigned T = kSegBatchGroups<G>;
+  // the bytes.  T groups per ticket (seg_batch_groups: as few as keep the
+  // single counter from serialising; one group whenever possible -- a batch
+  // of 8 long segments on one warp starved the others: 1023 x 64 KiB took
+  // 117 instead of 21 us)
+  const unsigned T = a.batch_groups;
   for (unsigned long long batch = gw;;) {
     if (batch * T * S >= a.nseg) break;
     for (unsigned tg = 0; tg < T; ++tg) {
@@ -647,10 +660,10 @@ cudaError_t launch_segmented(const SegArgs &a0, const DevInfo &di, cudaStream_t 
   const unsigned long long need = (a.nseg + segs_per_block - 1) / segs_per_block;
   const unsigned g = grid_for(need, (unsigned long long)di.num_sms * di.seg_blocks_per_sm);
   SegArgs b = a;  // dynamic group order once warps see several groups each
+  if (b.batch_groups == 0)
+    b.batch_groups = seg_batch_groups(a.nseg, G);
   // work units = the kernel's batches (its tickets)
-  const unsigned long long batches = G == 8    ? seg_batches<8>(a.nseg)
-                                     : G == 16 ? seg_batches<16>(a.nseg)
-                                               : seg_batches<32>(a.nseg);
+  const unsigned long long batches = seg_batches(a.nseg, G, b.batch_groups);
   std::unique_lock<std::mutex> lk;  // base hand-out and launch: one critical section
   if (need >= 4ull * g) {
     lk = sched_lock();

@@ -58,7 +58,7 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
     the lanes-per-segment launch shape.  By default it follows the segment
     lengths (host offsets, or device offsets with ``validate``): one lane per
     segment when every segment is at most LANE_MAX_BYTES, else G lanes by the
-    mean length; unknown lengths (device offsets, ``validate=False``) get the
+    byte-weighted mean length (_shape); unknown lengths (device offsets, ``validate=False``) get the
     C ABI default, G = 8.  ``hybrid=True`` adds a one-lane pass for the
     segments of at most LANE_MAX_BYTES (PP_SEG_HYBRID), which pays for
     strongly bimodal lengths.
@@ -79,7 +79,7 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
             if bool(((d & (step - 1)) != 0).any()):
                 raise InputLengthError(f"a segment is not a multiple of the {step}-byte word size")
             if lanes is None:  # validation already synchronised: pick the shape too
-                shape = _shape(int(d.numel()), int(d.max()), int(offs[-1] - offs[0]) // d.numel(),
+                shape = _shape(int(d.numel()), int(d.max()), _byte_mean(d),
                                _aligned_offsets(view, offs))
     else:
         offs_np = np.asarray(offsets, dtype=np.int64)
@@ -93,8 +93,7 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
                 raise InputLengthError(f"a segment is not a multiple of the {step}-byte word size")
         offs = torch.as_tensor(offs_np, device=dev)
         if lanes is None and offs_np.size > 1:
-            shape = _shape(int(d.size), int(d.max()),
-                           (int(offs_np[-1]) - int(offs_np[0])) // d.size,
+            shape = _shape(int(d.size), int(d.max()), _byte_mean(d),
                            _aligned_offsets(view, offs_np))
     nseg = offs.numel() - 1
     out, fresh = _out_tensor(out, max(nseg, 0), width, dev)
@@ -117,18 +116,33 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
     return out
 
 
-def _shape(nseg, dmax, mean, vec_aligned):
+def _byte_mean(d):
+    """Byte-weighted mean length sum(L^2) / sum(L): the length of the array
+    an average byte belongs to (numpy array or CUDA tensor of lengths)."""
+    if is_torch_tensor(d):
+        tot = int(d.sum())
+        return float((d.double() ** 2).sum()) / tot if tot else 0.0
+    d = np.asarray(d, dtype=np.float64)
+    tot = d.sum()
+    return float((d * d).sum() / tot) if tot else 0.0
+
+
+def _shape(nseg, dmax, bmean, vec_aligned):
     """Launch shape from the length distribution: (lanes, hybrid).
 
     Every array <= LANE_MAX_BYTES (LANE_MAX_ALIGNED when all arrays are
-    16-byte aligned): one lane each, else G lanes by the mean length.  The
-    hybrid split (PP_SEG_HYBRID, short arrays one lane each in a separate
-    pass) is opt-in: measured, it wins only for strongly bimodal lengths
-    (profiles/r1_segmented_ablation.md).
+    16-byte aligned): one lane each, else G lanes by the byte-weighted mean
+    length ``bmean`` (sum L^2 / sum L): G = 8 below 6 KiB, 16 below 10 KiB,
+    else 32 -- the best G over 11 length distributions, fixed, uniform,
+    exponential and log-normal (scripts/seg_shape_sweep.py,
+    profiles/r1_segmented_ablation.md); the count mean under-weights the
+    long arrays that carry most of the bytes.  The hybrid split
+    (PP_SEG_HYBRID, short arrays one lane each in a separate pass) is
+    opt-in: measured, it wins only for strongly bimodal lengths.
     """
     if dmax <= (LANE_MAX_ALIGNED if vec_aligned else LANE_MAX_BYTES):
         return 1, False
-    return (32 if mean >= 16384 else 16 if mean >= 8192 else 8), False
+    return (32 if bmean >= 10240 else 16 if bmean >= 6144 else 8), False
 
 
 def _aligned_offsets(view, offs):
@@ -184,7 +198,8 @@ def pospopcnt_batch(arrays, width, out=None, accumulate=True, lanes=None):
     tensors, all on one device, each word-complete.  Row i of the returned
     (n, width) int64 tensor is ``pospopcnt(arrays[i], width)``.  The launch
     shape follows the lengths (one lane per array when all are at most
-    LANE_MAX_BYTES, else G lanes by the mean length) unless ``lanes`` forces
+    LANE_MAX_BYTES, else G lanes by the byte-weighted mean length) unless
+    ``lanes`` forces
     it.  Asynchronous on the current stream (the pointer/length table is
     copied to the device once per call).
     """
@@ -220,9 +235,9 @@ def pospopcnt_batch(arrays, width, out=None, accumulate=True, lanes=None):
                                f"{step}-byte word size")
     out, fresh = _out_tensor(out, n, width, dev)
     if lanes is None:
-        dmax, mean = int(lens.max()), int(lens.sum()) // n
+        dmax = int(lens.max())
         aligned = not bool(((ptrs % 16) | (lens % 16)).any())
-        lanes = _shape(n, dmax, mean, aligned)[0]
+        lanes = _shape(n, dmax, _byte_mean(lens), aligned)[0]
     table = torch.from_numpy(np.concatenate([ptrs, lens]).view(np.int64)).to(dev)
     lib = _lib.load()
     flags = _lib.PP_SEG_ACCUMULATE if (accumulate and not fresh) else _lib.PP_SEG_OVERWRITE

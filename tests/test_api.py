@@ -251,3 +251,27 @@ def test_categories_and_segments_fail_loudly_without_gpu():
         pp.pospopcnt_categories(np.zeros(16, dtype=np.uint8), 12)
     with pytest.raises(ValueError):  # segmented counting needs device data
         pp.pospopcnt_segmented(b"\x00" * 16, [0, 8, 16], 8)
+
+
+def test_segmented_launch_shape_rule():
+    """Host-side shape rule of the segmented entry points: one lane per array
+    when every array is tiny, else G by the byte-weighted mean length
+    (profiles/r1_segmented_ablation.md)."""
+    import numpy as np
+    from paper_2412_16370_b200 import segmented as S
+    rng = np.random.default_rng(3)
+    K = 1024
+
+    def g(lens, aligned=False):
+        lens = np.asarray(lens, dtype=np.int64)
+        return S._shape(lens.size, int(lens.max()), S._byte_mean(lens), aligned)[0]
+
+    assert g(np.full(1000, 64)) == 1
+    assert g(np.full(1000, 4 * K)) == 8
+    assert g(np.full(1000, 8 * K)) == 16
+    assert g(np.full(1000, 16 * K)) == 32
+    assert g(rng.integers(0, 16 * K // 8, 100_000) * 8) == 32   # byte mean 10.7 KiB
+    assert g(rng.integers(4 * K // 8, 12 * K // 8, 100_000) * 8) == 16
+    assert g(rng.integers(0, 8 * K // 8, 100_000) * 8) == 8     # byte mean 5.3 KiB
+    assert S._byte_mean(np.array([0, 0])) == 0.0
+    assert S._byte_mean(np.array([2, 6])) == 5.0
