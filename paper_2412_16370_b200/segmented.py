@@ -47,7 +47,7 @@ def _out_tensor(out, nseg, width, device):
 
 
 def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validate=True,
-                        lanes=None, hybrid=False):
+                        lanes=None, hybrid=None):
     """Positional counts of many arrays in one launch.
 
     ``offsets``: nseg+1 non-decreasing byte offsets into the view (host
@@ -60,8 +60,9 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
     segment when every segment is at most LANE_MAX_BYTES, else G lanes by the
     byte-weighted mean length (_shape); unknown lengths (device offsets, ``validate=False``) get the
     C ABI default, G = 8.  ``hybrid=True`` adds a one-lane pass for the
-    segments of at most LANE_MAX_BYTES (PP_SEG_HYBRID), which pays for
-    strongly bimodal lengths.
+    segments of at most LANE_MAX_BYTES (PP_SEG_HYBRID), which pays when
+    most arrays are that small; ``None`` (default) lets the shape rule
+    decide when the lengths are known (``_shape``), ``False`` never.
     """
     import torch
     check_width(width)
@@ -80,7 +81,8 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
                 raise InputLengthError(f"a segment is not a multiple of the {step}-byte word size")
             if lanes is None:  # validation already synchronised: pick the shape too
                 shape = _shape(int(d.numel()), int(d.max()), _byte_mean(d),
-                               _aligned_offsets(view, offs))
+                               _aligned_offsets(view, offs),
+                               int((d <= LANE_MAX_BYTES).sum()))
     else:
         offs_np = np.asarray(offsets, dtype=np.int64)
         if offs_np.ndim != 1 or offs_np.size < 1:
@@ -94,7 +96,8 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
         offs = torch.as_tensor(offs_np, device=dev)
         if lanes is None and offs_np.size > 1:
             shape = _shape(int(d.size), int(d.max()), _byte_mean(d),
-                           _aligned_offsets(view, offs_np))
+                           _aligned_offsets(view, offs_np),
+                           int(np.count_nonzero(d <= LANE_MAX_BYTES)))
     nseg = offs.numel() - 1
     out, fresh = _out_tensor(out, max(nseg, 0), width, dev)
     if nseg <= 0:
@@ -103,6 +106,8 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
     flags = _lib.PP_SEG_ACCUMULATE if (accumulate and not fresh) else _lib.PP_SEG_OVERWRITE
     if lanes is None and shape is not None:
         lanes = shape[0]
+        if hybrid is None:
+            hybrid = shape[1]
     if hybrid:
         flags |= _lib.PP_SEG_HYBRID
     flags |= _lanes_flag(lanes)
@@ -127,7 +132,7 @@ def _byte_mean(d):
     return float((d * d).sum() / tot) if tot else 0.0
 
 
-def _shape(nseg, dmax, bmean, vec_aligned):
+def _shape(nseg, dmax, bmean, vec_aligned, nshort=0):
     """Launch shape from the length distribution: (lanes, hybrid).
 
     Every array <= LANE_MAX_BYTES (LANE_MAX_ALIGNED when all arrays are
@@ -136,12 +141,17 @@ def _shape(nseg, dmax, bmean, vec_aligned):
     else 32 -- the best G over 11 length distributions, fixed, uniform,
     exponential and log-normal (scripts/seg_shape_sweep.py,
     profiles/r1_segmented_ablation.md); the count mean under-weights the
-    long arrays that carry most of the bytes.  The hybrid split
-    (PP_SEG_HYBRID, short arrays one lane each in a separate pass) is
-    opt-in: measured, it wins only for strongly bimodal lengths.
+    long arrays that carry most of the bytes.  When at least 60 % of the
+    arrays (``nshort`` of ``nseg``) are at most LANE_MAX_BYTES: the hybrid
+    split (PP_SEG_HYBRID: those one lane each in a separate pass) with
+    G = 32 for the rest, which skips whole short groups (measured best on
+    every such mix, 1.1-1.7x faster: scripts/seg_hybrid_sweep.py); at 50 %
+    the split no longer pays.
     """
     if dmax <= (LANE_MAX_ALIGNED if vec_aligned else LANE_MAX_BYTES):
         return 1, False
+    if nseg and nshort >= 0.6 * nseg:
+        return 32, True
     return (32 if bmean >= 10240 else 16 if bmean >= 6144 else 8), False
 
 

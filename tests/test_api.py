@@ -275,3 +275,20 @@ def test_segmented_launch_shape_rule():
     assert g(rng.integers(0, 8 * K // 8, 100_000) * 8) == 8     # byte mean 5.3 KiB
     assert S._byte_mean(np.array([0, 0])) == 0.0
     assert S._byte_mean(np.array([2, 6])) == 5.0
+
+
+def test_segmented_hybrid_rule():
+    """Mostly-tiny arrays take the hybrid split with G = 32 for the rest."""
+    import numpy as np
+    from paper_2412_16370_b200 import segmented as S
+    rng = np.random.default_rng(4)
+
+    def shape(lens):
+        lens = np.asarray(lens, dtype=np.int64)
+        return S._shape(lens.size, int(lens.max()), S._byte_mean(lens), False,
+                        int(np.count_nonzero(lens <= S.LANE_MAX_BYTES)))
+
+    assert shape(np.where(rng.random(10_000) < 0.9, 64, 16384)) == (32, True)
+    assert shape(np.where(rng.random(10_000) < 0.7, 256, 4096)) == (32, True)
+    assert shape(np.where(rng.random(10_000) < 0.5, 512, 2048)) == (8, False)
+    assert shape(np.full(100, 256)) == (1, False)
