@@ -35,6 +35,9 @@ STALLS = "smsp__pcsamp_warps_issue_stalled_"
 
 
 def short(name):
+    for w in (8, 16, 32, 64):  # categories kernels carry a third (code-bytes) parameter
+        if f"pp_tma_kernel<{w}, 16, 1>" in name:
+            return f"pp_tma_kernel<{w}, 16>"
     for k in ("pp_tma_kernel<32, 16>", "pp_tma_kernel<8, 16>", "pp_tma_kernel<16, 16>",
               "pp_tma_kernel<64, 16>", "pp_tma_kernel<1,", "pp_tma_kernel<0,",
               "pp_tma_kernel<1>", "pp_tma_kernel<0>", "pp_tma_kernel<true>", "pp_tma_kernel<false>",
