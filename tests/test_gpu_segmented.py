@@ -192,3 +192,30 @@ def test_batch_of_separate_arrays(cuda, oracle, rng, lanes):
         assert np.array_equal(out.cpu().numpy().view(np.uint64), 2 * got)
     with pytest.raises(pp.InputLengthError):
         pp.pospopcnt_batch([torch.zeros(3, dtype=torch.uint8, device="cuda")], 16)
+
+
+def test_ticket_batches_many_segments(cuda, oracle):
+    """Launches with more than 49,152 groups batch T > 1 groups per scheduler
+    ticket (seg_batch_groups); explicit PP_SEG_BATCH hints 1 / 5 / 63 too.
+    Every shape must stay exact, including a last batch that is partial."""
+    torch, pp = cuda
+    from paper_2412_16370_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(31)
+    nseg = 300_007
+    lens = rng.integers(0, 2048 // 8, nseg) * 8
+    offs = np.zeros(nseg + 1, dtype=np.int64)
+    offs[1:] = np.cumsum(lens)
+    host = rng.integers(0, 256, int(offs[-1]) + 16, dtype=np.uint8)
+    buf = torch.from_numpy(host).cuda()
+    d = torch.from_numpy(offs).cuda()
+    want = oracle.segments(host, offs.astype(np.uint64), 64)
+    out = torch.empty((nseg, 64), dtype=torch.int64, device="cuda")
+    sp = torch.cuda.current_stream().cuda_stream
+    for lanes in (8, 16, 32):
+        for t in (0, 1, 5, 63):
+            out.fill_(-1)
+            fl = _lib.PP_SEG_OVERWRITE | (lanes << 8) | (t << _lib.PP_SEG_BATCH_SHIFT)
+            _lib.check(lib.pp_count_segmented(buf.data_ptr(), d.data_ptr(), nseg, 64,
+                                              out.data_ptr(), fl, sp))
+            assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (lanes, t)
