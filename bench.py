@@ -290,7 +290,7 @@ def run_reference(args):
                 "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -693,7 +693,7 @@ def main_gpu(args):
             "per_width_gbs": per_width,
             "c4_short_sweep": c4_sweep,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if peers is not None:
         peers.sync()
         peers.close()
@@ -702,7 +702,29 @@ def main_gpu(args):
     return 0
 
 
+_JSON_OUT = None  # the real stdout: the one JSON line goes here, nothing else
+
+
+def claim_stdout():
+    """Point fd 1 at stderr for the rest of the run and keep a private copy
+    of the real stdout for the JSON line: NCCL (e.g. NCCL_DEBUG=VERSION prints
+    "NCCL version ..." on stdout at init), CUDA or torch messages must not
+    mix into the one line the driver parses."""
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line):
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)

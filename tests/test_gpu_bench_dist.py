@@ -41,8 +41,10 @@ def test_bench_two_ranks_one_gpu(cuda, config, exchange):
            "--config", config, "--exchange", exchange, "--no-e2e", "--no-cpu-baseline"]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
-    lines = [json.loads(x) for x in res.stdout.splitlines() if x.startswith("{")]
-    assert len(lines) == 1, res.stdout[-3000:]
+    # stdout carries exactly one line, the JSON (NCCL / torch chatter -> stderr)
+    out = [x for x in res.stdout.splitlines() if x.strip()]
+    assert len(out) == 1 and out[0].startswith("{"), res.stdout[-3000:]
+    lines = [json.loads(out[0])]
     line = lines[0]
     assert line["n_gpus"] == 2 and line["exact"] is True, line
     assert line["config"]["bytes_per_step_all_gpus"] == (
