@@ -47,6 +47,7 @@ sys.path.insert(0, ROOT)
 METRIC = "pospopcnt input GB/s (fraction of HBM peak) at 1/2/4/8 B200, per word width"
 GIB = 1 << 30
 MIB = 1 << 20
+SPEC_HBM_GBS = 7700.0  # B200 HBM3e datasheet bandwidth (HGX figure; B200_PROFILING.md)
 SETTLE_MS = 30.0  # untimed device work after the W warm-up steps (see main_gpu)
 
 CONFIGS = {
@@ -627,7 +628,10 @@ def main_gpu(args):
                 "kernel": kernel_key, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": per_step_bytes,
                 "traffic_per_input_byte_ncu": traffic_ratio,
-                "readonly_roofline_gbs": round(ro_gbs, 1)}
+                "readonly_roofline_gbs": round(ro_gbs, 1),
+                # B200 HBM3e datasheet figure (HGX; 8 TB/s DGX), stated as such
+                "spec_peak_gbs": SPEC_HBM_GBS,
+                "frac_of_spec": round(achieved / SPEC_HBM_GBS, 4)}
     if seg_out is not None:
         seg_bytes_out = (nbytes // 4096) * w * 8
         roofline["algorithmic_bytes_per_launch"] = per_step_bytes + seg_bytes_out
