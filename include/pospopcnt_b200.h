@@ -124,6 +124,19 @@ PP_API int pp_count_segmented(const void *base, const unsigned long long *seg_of
                        int flags, void *stream);
 
 /*
+ * pp_count_segmented_order — pp_count_segmented processing the segments in a
+ * caller-given order: order (DEVICE, nseg uint32, a permutation of 0..nseg-1)
+ * lists segment indices in the order the G-lane kernel takes them, in groups
+ * of 32/G; rows still land at out[s].  With the segments of each group of
+ * similar length (segmented.SegmentPlan sorts by length and alternates long
+ * and short groups) no lane idles while a longer neighbour finishes.
+ * Applies to the G-lane kernel (G = 8/16/32); the one-lane pass ignores it.
+ */
+PP_API int pp_count_segmented_order(const void *base, const unsigned long long *seg_off,
+                                    const unsigned int *order, size_t nseg, int width,
+                                    unsigned long long *out, int flags, void *stream);
+
+/*
  * pp_count_batch — many independent arrays at arbitrary device addresses in
  * one launch: row i of out (DEVICE, n*width uint64, row-major) receives the
  * count of bytes [ptrs[i], ptrs[i] + lens[i]).  ptrs / lens are DEVICE

@@ -42,6 +42,7 @@ SIGNATURES = {
     "pp_ipc_close": (_int, [_vp]),
     "pp_count_categories": (_int, [_vp, _sz, _int, _int, _vp, _vp]),
     "pp_count_segmented": (_int, [_vp, _vp, _sz, _int, _vp, _int, _vp]),
+    "pp_count_segmented_order": (_int, [_vp, _vp, _vp, _sz, _int, _vp, _int, _vp]),
     "pp_count_fixed": (_int, [_vp, _sz, _sz, _int, _vp, _int, _vp]),
     "pp_count_batch": (_int, [_vp, _vp, _sz, _int, _vp, _int, _vp]),
     "pp_readonly_sum": (_int, [_vp, _sz, _vp, _vp]),

@@ -345,6 +345,28 @@ int pp_count_segmented(const void *base, const unsigned long long *seg_off, size
   return seg_common(a, stream);
 }
 
+int pp_count_segmented_order(const void *base, const unsigned long long *seg_off,
+                             const unsigned int *order, size_t nseg, int width,
+                             unsigned long long *out, int flags, void *stream) {
+  if (!seg_off && nseg) return fail(PP_EARG, "seg_off is NULL");
+  if (!order && nseg) return fail(PP_EARG, "order is NULL");
+  if (nseg > 0xFFFFFFFFull) return fail(PP_EARG, "order holds 32-bit indices: nseg < 2^32");
+  int rc;
+  if (nseg && (rc = check_device_ptr(order, "order"))) return rc;
+  pp::SegArgs a{};
+  a.base = static_cast<const uint8_t *>(base);
+  a.seg_off = seg_off;
+  a.order = order;
+  a.nseg = nseg;
+  a.out = out;
+  a.width = width;
+  a.overwrite = (flags & PP_SEG_OVERWRITE) ? 1 : 0;
+  a.batch_groups = seg_batch_hint(flags);
+  a.lanes_per_segment = seg_lanes(flags, kUnknownLengthBytes);
+  if ((flags & PP_SEG_HYBRID) && a.lanes_per_segment != 1) a.short_max = kLaneAutoMaxBytes;
+  return seg_common(a, stream);
+}
+
 int pp_count_batch(const unsigned long long *ptrs, const unsigned long long *lens, size_t n,
                    int width, unsigned long long *out, int flags, void *stream) {
   if (!width_ok(width)) return fail(PP_EWIDTH, "word width must be one of (8, 16, 32, 64), got %d", width);

@@ -55,6 +55,9 @@ struct SegArgs {
   // device arrays of absolute addresses and byte lengths; base/seg_off unused
   const unsigned long long *ptrs;
   const unsigned long long *lens;
+  // processing order of the G-lane kernel (pp_count_segmented_order): slot k
+  // counts segment order[k]; nullptr = slot k is segment k
+  const unsigned int *order;
 };
 
 enum class LoadPath : int { kTma = 0, kLdg = 1 };

@@ -210,9 +210,11 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
     for (unsigned tg = 0; tg < T; ++tg) {
       const unsigned long long first = (batch * T + tg) * S;
       if (first >= a.nseg) break;
-      const unsigned long long s = first + sl;
+      const unsigned long long slot = first + sl;
+      // the segment this slot counts (caller-given order, else the slot)
+      const unsigned long long s = (a.order && slot < a.nseg) ? a.order[slot] : slot;
       SegGeom g = seg_geom(a, s);
-      bool mine = s < a.nseg;
+      bool mine = slot < a.nseg;
       if (HYBRID) {  // short segments belong to the one-lane kernel
         mine = mine && g.e - g.p0 > a.short_max;
         if (!mine) g.nvv = 0;

@@ -47,7 +47,7 @@ def _out_tensor(out, nseg, width, device):
 
 
 def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validate=True,
-                        lanes=None, hybrid=None):
+                        lanes=None, hybrid=None, plan=None):
     """Positional counts of many arrays in one launch.
 
     ``offsets``: nseg+1 non-decreasing byte offsets into the view (host
@@ -63,10 +63,15 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
     segments of at most LANE_MAX_BYTES (PP_SEG_HYBRID), which pays when
     most arrays are that small; ``None`` (default) lets the shape rule
     decide when the lengths are known (``_shape``), ``False`` never.
+    ``plan``: a ``SegmentPlan`` built once for these offsets (repeated counts
+    over one segmentation): the G-lane kernel then takes the segments in the
+    plan's length-sorted order and the plan's shape; ``offsets`` may be None.
     """
     import torch
     check_width(width)
     view = _device_view(data)
+    if plan is not None:
+        return plan.count(view, width, out=out, accumulate=accumulate)
     dev = view.base.device
     step = width // 8
     shape = None  # (lanes, hybrid) from the lengths, when they are known here
@@ -171,6 +176,110 @@ def _lanes_flag(lanes):
     if lanes not in (1, 2, 4, 8, 16, 32):
         raise ValueError("lanes must be 1, 2, 4, 8, 16 or 32")
     return lanes << 8
+
+
+class SegmentPlan:
+    """A reusable launch plan for one CSR segmentation (offsets), for callers
+    that count many inputs with the same layout.
+
+    Ragged lengths leave lanes idle: a G-lane group of 32/G segments runs as
+    long as its longest member.  The plan sorts the segments by length and
+    groups neighbours in that order, so each group's segments have similar
+    lengths; groups are then taken long, short, long, short, ... (longest
+    first for the tail, and streaming-bound long groups interleaved with
+    flush-bound short ones).  ``count`` launches pp_count_segmented_order;
+    rows still land at their segment's index.  The shape (lanes, hybrid)
+    comes from ``_shape`` (one lane for all-tiny arrays, the hybrid split for
+    mostly-tiny ones) with G = 8 / 16 / 32 below 17 / 34 KiB / above of
+    byte-weighted mean length, unless ``lanes`` forces it.  Measured vs the
+    index order (1 GiB, w=64): uniform 0-4 KiB 373 -> 312 us, exponential
+    mean 2 KiB 414 -> 312, mean 4 KiB 294 -> 241 (best G each side).
+    """
+
+    def __init__(self, offsets, device=None, lanes=None, hybrid=None):
+        import torch
+        if is_torch_tensor(offsets):
+            device = offsets.device if offsets.is_cuda else device
+            offs_np = offsets.detach().cpu().numpy().astype(np.int64)
+        else:
+            offs_np = np.asarray(offsets, dtype=np.int64)
+        if offs_np.ndim != 1 or offs_np.size < 1:
+            raise ValueError("offsets must be a 1-D sequence of nseg+1 byte offsets")
+        d = np.diff(offs_np)
+        if (d < 0).any() or offs_np[0] < 0:
+            raise ValueError("offsets must be non-decreasing and non-negative")
+        self.nseg = int(d.size)
+        if self.nseg >= 1 << 32:
+            raise ValueError("a plan holds 32-bit segment indices")
+        self.end = int(offs_np[-1])
+        # OR of all lengths: word-complete for w iff its low log2(w/8) bits are 0
+        self._len_or = int(np.bitwise_or.reduce(d)) if d.size else 0
+        if self.nseg:
+            bm = _byte_mean(d)
+            shp = _shape(self.nseg, int(d.max()), bm, False,
+                         int(np.count_nonzero(d <= LANE_MAX_BYTES)))
+            if shp[0] != 1 and not shp[1]:
+                # balanced groups: 8 lanes per segment stay best to a larger
+                # byte mean than in index order (scripts/seg_plan_probe.py)
+                shp = (8 if bm < 17 * 1024 else 16 if bm < 34 * 1024 else 32), False
+        else:
+            shp = (8, False)
+        self.lanes = lanes if lanes is not None else shp[0]
+        self.hybrid = shp[1] if hybrid is None else bool(hybrid)
+        if self.lanes == 1 or self.hybrid:
+            # the one-lane kernel takes segments in index order; with the
+            # hybrid split the sorted order measured slower (90 % 64 B /
+            # 16 KiB: 310 vs 285 us), the G pass skips the tiny groups anyway
+            order = np.arange(self.nseg, dtype=np.uint32)
+        else:
+            order = self._order(d, 32 // self.lanes)
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        if dev.type == "cuda" and dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        self.offsets = torch.as_tensor(offs_np, device=dev)
+        self.order = torch.as_tensor(order.view(np.int32), device=dev)
+
+    @staticmethod
+    def _order(d, S):
+        """Segment indices by descending length, cut into groups of S, the
+        full groups taken alternately from the long and the short end, the
+        partial group (if any: the S shortest-but-remaining) last."""
+        idx = np.argsort(-d, kind="stable").astype(np.uint32)
+        nfull = idx.size // S
+        full = idx[: nfull * S].reshape(nfull, S)
+        g = np.empty(nfull, dtype=np.int64)
+        g[0::2] = np.arange((nfull + 1) // 2)
+        g[1::2] = nfull - 1 - np.arange(nfull // 2)
+        return np.concatenate([full[g].reshape(-1), idx[nfull * S:]])
+
+    def count(self, data, width, out=None, accumulate=True):
+        """Positional counts of the plan's segments of ``data`` (as
+        pospopcnt_segmented).  Asynchronous on the current stream."""
+        import torch
+        check_width(width)
+        view = _device_view(data)
+        if view.base.device != self.device:
+            raise ValueError("data and plan live on different devices")
+        if self.end > view.nbytes:
+            raise ValueError("the plan's offsets run past the view")
+        if self._len_or & (width // 8 - 1):
+            raise InputLengthError(f"a segment is not a multiple of the {width // 8}-byte "
+                                   "word size")
+        out, fresh = _out_tensor(out, self.nseg, width, self.device)
+        if self.nseg == 0:
+            return out
+        lib = _lib.load()
+        flags = _lib.PP_SEG_ACCUMULATE if (accumulate and not fresh) else _lib.PP_SEG_OVERWRITE
+        if self.hybrid:
+            flags |= _lib.PP_SEG_HYBRID
+        flags |= _lanes_flag(self.lanes)
+        with torch.cuda.device(self.device):
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+            _lib.check(lib.pp_count_segmented_order(
+                view.base.data_ptr() + view.offset, self.offsets.data_ptr(),
+                self.order.data_ptr(), self.nseg, width, out.data_ptr(), flags, stream))
+        return out
 
 
 def pospopcnt_fixed(data, seg_bytes, width, out=None, accumulate=True, lanes=None):

@@ -292,3 +292,46 @@ def test_segmented_hybrid_rule():
     assert shape(np.where(rng.random(10_000) < 0.7, 256, 4096)) == (32, True)
     assert shape(np.where(rng.random(10_000) < 0.5, 512, 2048)) == (8, False)
     assert shape(np.full(100, 256)) == (1, False)
+
+
+def test_segment_plan_order():
+    """SegmentPlan's processing order: a permutation; each full group of
+    32/G slots holds segments adjacent in length-sorted order; long and short
+    groups alternate; the partial group goes last."""
+    import numpy as np
+    from paper_2412_16370_b200.segmented import SegmentPlan
+    rng = np.random.default_rng(9)
+    d = rng.integers(0, 5000, 1003)
+    for S in (1, 2, 4):
+        order = SegmentPlan._order(d, S)
+        assert sorted(order.tolist()) == list(range(d.size))
+        rank = np.empty(d.size, dtype=np.int64)
+        rank[np.argsort(-d, kind="stable")] = np.arange(d.size)
+        nfull = d.size // S
+        groups = rank[order[: nfull * S]].reshape(nfull, S)
+        assert (groups.max(1) - groups.min(1) == S - 1).all()  # neighbours in sorted order
+        first = groups.min(1) // S  # the sorted group each slot group came from
+        assert first[0] == 0 and (nfull < 2 or first[1] == nfull - 1)
+        assert sorted(first.tolist()) == list(range(nfull))
+        assert set(rank[order[nfull * S:]].tolist()) == set(range(nfull * S, d.size))
+
+
+def test_segment_plan_shape():
+    """SegmentPlan's shape rule (built on the CPU: no launch needed)."""
+    import numpy as np
+    from paper_2412_16370_b200.segmented import SegmentPlan
+    rng = np.random.default_rng(10)
+    K = 1024
+
+    def plan(lens):
+        offs = np.zeros(len(lens) + 1, dtype=np.int64)
+        offs[1:] = np.cumsum(lens)
+        return SegmentPlan(offs, device="cpu")
+
+    assert plan(rng.integers(0, 16 * K // 8, 20_000) * 8).lanes == 8    # byte mean 10.7 K
+    assert plan(rng.integers(0, 32 * K // 8, 20_000) * 8).lanes == 16   # 21 K
+    assert plan(np.full(1000, 64 * K)).lanes == 32
+    p = plan(np.where(rng.random(20_000) < 0.9, 64, 16 * K))
+    assert (p.lanes, p.hybrid) == (32, True)
+    assert plan(np.full(1000, 256)).lanes == 1
+    assert plan(np.full(10, 4096)).order.numel() == 10

@@ -219,3 +219,35 @@ def test_ticket_batches_many_segments(cuda, oracle):
             _lib.check(lib.pp_count_segmented(buf.data_ptr(), d.data_ptr(), nseg, 64,
                                               out.data_ptr(), fl, sp))
             assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (lanes, t)
+
+
+@pytest.mark.parametrize("lanes", (None, 8, 16, 32))
+def test_segment_plan_exact(cuda, oracle, lanes):
+    """SegmentPlan (length-sorted processing order, pp_count_segmented_order)
+    must give the same rows as the plain segmented count: ragged lengths
+    incl. empty, tiny (hybrid pass) and long segments, misaligned base,
+    overwrite and accumulate, every width."""
+    torch, pp = cuda
+    rng = np.random.default_rng(77)
+    for w in (8, 16, 32, 64):
+        step = w // 8
+        lens = np.concatenate([rng.integers(0, 8192 // step, 20_000) * step,
+                               np.zeros(7, np.int64), np.full(50, 3 * step),
+                               rng.integers(0, 300_000 // step, 40) * step])
+        rng.shuffle(lens)
+        offs = np.zeros(lens.size + 1, dtype=np.int64)
+        offs[1:] = np.cumsum(lens)
+        base = 3
+        host = rng.integers(0, 256, int(offs[-1]) + base + 5, dtype=np.uint8)
+        buf = torch.from_numpy(host).cuda()
+        view = pp.InputView(buf, base, int(offs[-1]))
+        want = oracle.segments(host, (offs + base).astype(np.uint64), w)
+        plan = pp.SegmentPlan(offs, device="cuda", lanes=lanes)
+        out = pp.pospopcnt_segmented(view, None, w, plan=plan)
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (w, plan.lanes)
+        plan.count(view, w, out=out)  # accumulate
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), 2 * want), w
+        tiny = pp.SegmentPlan(np.where(rng.random(5000) < 0.9, 64, 4096).cumsum(), device="cuda")
+        assert tiny.hybrid and tiny.lanes == 32
+    with pytest.raises(ValueError):
+        pp.SegmentPlan([0, 8, 4])
