@@ -49,17 +49,27 @@ def one_case(rng, dev_buf, host, stream):
                 want = O.hs512(host, off, min(n, 8 * MIB) // step * step, w, threads=4)
             return kind, (w, n, off), got == want
         if kind == "seg":
-            nseg = rng.randrange(1, 3000)
-            lens = [rng.choice((0, step, 7 * step, rng.randrange(0, 5000) // step * step,
-                                rng.randrange(0, 70000) // step * step)) for _ in range(nseg)]
+            if rng.random() < 0.9:
+                nseg = rng.randrange(1, 3000)
+                lens = [rng.choice((0, step, 7 * step, rng.randrange(0, 5000) // step * step,
+                                    rng.randrange(0, 70000) // step * step)) for _ in range(nseg)]
+            else:  # enough groups for scheduler batches of T > 1
+                nseg = rng.randrange(50_000, 120_000)
+                lens = (np.random.default_rng(rng.randrange(1 << 30)).integers(0, 4096 // step, nseg)
+                        * step).tolist()
             offs = np.zeros(nseg + 1, dtype=np.int64)
             offs[1:] = np.cumsum(lens)
             if offs[-1] + off > host.size:
                 return kind, "skip", True
             lanes = rng.choice((None, None, 1, 8, 16, 32))
-            hybrid = rng.random() < 0.2
-            out = pp.pospopcnt_segmented(pp.InputView(dev_buf, off, int(offs[-1])), offs, w,
-                                         lanes=lanes, hybrid=hybrid)
+            hybrid = rng.choice((None, False, True))
+            view = pp.InputView(dev_buf, off, int(offs[-1]))
+            if rng.random() < 0.3:  # a SegmentPlan (length-sorted order)
+                plan = pp.SegmentPlan(offs, device="cuda", lanes=lanes, hybrid=hybrid)
+                out = pp.pospopcnt_segmented(view, None, w, plan=plan)
+                lanes = ("plan", plan.lanes)
+            else:
+                out = pp.pospopcnt_segmented(view, offs, w, lanes=lanes, hybrid=hybrid)
             want = O.segments(host, (offs + off).astype(np.uint64), w, threads=4)
             return kind, (w, nseg, off, lanes, hybrid), np.array_equal(
                 out.cpu().numpy().view(np.uint64), want)
