@@ -48,7 +48,9 @@ METRIC = "pospopcnt input GB/s (fraction of HBM peak) at 1/2/4/8 B200, per word 
 GIB = 1 << 30
 MIB = 1 << 20
 SPEC_HBM_GBS = 7700.0  # B200 HBM3e datasheet bandwidth (HGX figure; B200_PROFILING.md)
-SETTLE_MS = 30.0  # untimed device work after the W warm-up steps (see main_gpu)
+SETTLE_MS = 30.0
+L2_FLUSH_BELOW = 256 * MIB  # inputs below this may stay in the 126 MB L2: flush per step
+L2_FLUSH_BYTES = 512 * MIB  # untimed device work after the W warm-up steps (see main_gpu)
 
 CONFIGS = {
     # name: (generator, width, bytes per GPU (weak) or in total (strong), description)
@@ -455,23 +457,45 @@ def main_gpu(args):
         dist.barrier()
     torch.cuda.synchronize()
 
+    # inputs that fit in the 126 MB L2 (C1, C4): flush L2 before every step
+    # (write a buffer larger than L2) and time each step alone with its own
+    # event pair -- the sum of those is the timed region; larger inputs
+    # stream past L2 and are timed as K back-to-back steps
+    flush_l2 = nbytes < L2_FLUSH_BELOW
+    flush_buf = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev) if flush_l2 else None
+    flush_sink = torch.zeros((), dtype=torch.int64, device=dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         time.sleep(0.05)  # let the sampler start before the timed region
         clk.mark(True)
-        gpu_busy()  # launches queue behind a spin, not an idle GPU
-        e0.record(st)
-        for _ in range(args.steps):
-            step()
-        drain()
-        e1.record(st)
+        if flush_l2:
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            for a_ev, b_ev in evs:
+                # write the flush buffer, then read it: L2 ends up holding
+                # clean lines of it (a write alone leaves ~126 MB of dirty
+                # lines whose write-back would land inside the timed step)
+                flush_buf.fill_(1)
+                flush_sink.copy_(flush_buf.view(torch.int64).max())
+                a_ev.record(st)
+                step()
+                b_ev.record(st)
+            drain()
+        else:
+            gpu_busy()  # launches queue behind a spin, not an idle GPU
+            e0.record(st)
+            for _ in range(args.steps):
+                step()
+            drain()
+            e1.record(st)
         torch.cuda.synchronize()
         clk.mark(False)
     if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
-    t_ms = e0.elapsed_time(e1)
-    if not use_dist or fused:
+    t_ms = sum(a_ev.elapsed_time(b_ev) for a_ev, b_ev in evs) if flush_l2 else e0.elapsed_time(e1)
+    del flush_buf
+    if not use_dist or fused or flush_l2:
         # each step is exactly one launch of the dominant kernel
         k_ms = t_ms / args.steps
     else:
@@ -562,7 +586,8 @@ def main_gpu(args):
     # BASELINE config 4 at byte offsets 1..7 (latency-bound below ~16 MiB)
     c4_sweep = None
     if cfg == "c4":
-        c4_sweep = {}
+        c4_sweep = {"_note": "per-call device latency, launches queued back to back over the "
+                             "same buffer (L2 warm; the sizes below 1 MiB are launch-bound)"}
         scratch_c = torch.zeros(64, dtype=torch.int64, device=dev)
         for words in (1, 3, 17, 255, 512, 8192, 131072, 8388608):
             nb = 8 * words
@@ -707,8 +732,10 @@ def main_gpu(args):
                                        "per step)") if world > 1 else "single GPU",
                        "settle": f"{n_settle + 1} untimed launches (>= {SETTLE_MS:.0f} ms) "
                                  "after the warm-up steps, into scratch counters",
-                       "l2": "input >> 126 MB L2, no flush needed" if nbytes > 256 * MIB
-                             else "input fits L2 (reported, not judged vs HBM)"},
+                       "l2": "input >> 126 MB L2, no flush needed" if not flush_l2
+                             else f"L2 flushed before every step ({L2_FLUSH_BYTES >> 20} MiB "
+                                  "written then read), each step timed alone with its own "
+                                  "CUDA events"},
             "hbm_frac": round(value / world / peak, 4),
             "exact_reference": "C5: reference numba total of the 64 GiB array (golden.json)"
                                if cfg == "c5" else "CPU oracle (C port of NumbaKernel.run) "
