@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
       // the segment this slot counts (caller-given order, else the slot)
       const unsigned long long s = (a.order && slot < a.nseg) ? a.order[slot] : slot;
       SegGeom g = seg_geom(a, s);
-      bool mine = slot < a.nseg;
+      bool mine = slot < a.nseg && s < a.nseg;  // (an out-of-range order entry writes nothing)
       if (HYBRID) {  // short segments belong to the one-lane kernel
         mine = mine && g.e - g.p0 > a.short_max;
         if (!mine) g.nvv = 0;
