@@ -553,6 +553,19 @@ def main_gpu(args):
                           dtype=torch.int64, device=dev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         exact = bool(ok.item())
+    elif args.check and seg_out is not None:
+        # every row of this rank's segments against the oracle's per-segment
+        # count (rows were overwritten by each step: one pass)
+        from oracle import oracle as O
+        host = buf[:nbytes].cpu().numpy()
+        offs = np.arange(nbytes // 4096 + 1, dtype=np.uint64) * 4096
+        want = O.segments(host, offs, w, threads=max(1, host_threads() // world))
+        exact = bool(np.array_equal(seg_out.cpu().numpy().view(np.uint64), want))
+        if use_dist:
+            ok = torch.tensor([int(exact)], dtype=torch.int64, device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            exact = bool(ok.item())
+        del host
     elif args.check and cfg in ("c1", "c2", "c3", "c4") and rank == 0:
         from oracle import oracle as O
         host = buf.cpu().numpy()
