@@ -18,8 +18,14 @@ torch.cuda.synchronize()
 tl = np.zeros((1024, 8), dtype=np.uint64)
 f = lib.pp_debug_timeline
 f.argtypes = [ctypes.c_void_p]
-for label, k in (("alone", 1), ("back-to-back (last of 10)", 10)):
-    torch.cuda._sleep(1000000)
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+sink = torch.zeros((), dtype=torch.int64, device="cuda")
+for label, k in (("alone", 1), ("back-to-back (last of 10)", 10), ("cold (L2 flushed)", 1)):
+    if label.startswith("cold"):
+        flush.fill_(1)
+        sink.copy_(flush.view(torch.int64).max())
+    else:
+        torch.cuda._sleep(1000000)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(k):
