@@ -1,0 +1,53 @@
+"""bench.py's JSON line carries every key of the driver's contract (and the
+reference arm's), with consistent values -- run on the GPU box."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(*args):
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert res.returncode == 0, res.stderr[-3000:]
+    out = [x for x in res.stdout.splitlines() if x.strip()]
+    assert len(out) == 1, res.stdout
+    return json.loads(out[0])
+
+
+def test_bench_line_contract(cuda):
+    d = _run("--steps", "5", "--warmup", "3", "--cpu-min-time", "0.5")
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3
+    assert d["unit"] == "GB/s" and d["higher_is_better"] is True and d["dtype"] == "u8"
+    assert d["value"] > 1000 and d["exact"] is True
+    assert abs(d["value"] - d["config"]["bytes_per_step_all_gpus"] / d["ms_per_step"] / 1e6) \
+        < 0.01 * d["value"]
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["peak"] > 0
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
+    c = d["cpu_baseline"]
+    assert c["kind"] == "port" and c["cores"] >= 1 and c["value"] > 0 and c["sample"]
+    e = d["e2e"]
+    assert e["unit"] == "GB/s" and e["value"] > 0
+    assert e["h2d_bytes_per_step"] == d["config"]["bytes_per_gpu_per_step"]
+    assert e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] == 5
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    assert "workload" in d["config"]
+
+
+def test_reference_arm_contract():
+    d = _run("--impl", "reference", "--steps", "1", "--warmup", "3")
+    assert d["impl"] == "reference" and d["unit"] == "GB/s" and d["value"] > 0
+    assert d["cpu_baseline"]["value"] == d["value"] and d["e2e"]["value"] == d["value"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["gpu_launches"] == 0
