@@ -34,7 +34,10 @@ namespace pp {
 #ifndef PP_TIMELINE
 #define PP_TIMELINE 0
 #endif
-constexpr int kTmaConsumerWarps = 8;
+#ifndef PP_TMA_NCW
+#define PP_TMA_NCW 8
+#endif
+constexpr int kTmaConsumerWarps = PP_TMA_NCW;
 constexpr int kSchedSlotsAlloc = 256;  // = kSchedSlots (scheduler slots per device)
 #ifndef PP_TMA_STAGES
 #define PP_TMA_STAGES 3
