@@ -45,3 +45,12 @@ def test_kernels_listing(capsys):
     lines = out.strip().splitlines()
     assert lines[0].startswith("b200")
     assert all(("available" in ln or "unavailable" in ln) for ln in lines)
+
+
+def test_selftest_without_gpu_is_an_input_error(capsys, monkeypatch):
+    """No usable kernel: KernelUnavailableError -> exit 2 (cli.py:151-154);
+    never a silent CPU run."""
+    from paper_2412_16370_b200 import kernels as K
+    monkeypatch.setattr(K.B200Kernel, "available", lambda self: False)
+    code, _, err = run(capsys, "selftest", "--iterations", "3")
+    assert code == 2 and ("not available" in err or "no pospopcnt kernel" in err)
