@@ -123,6 +123,27 @@ __device__ __noinline__ uint4 load_edge(uintptr_t va, uintptr_t p0, uintptr_t e,
   return load_partial(va, p0, e);
 }
 
+#ifndef PP_ROW_STREAM
+#define PP_ROW_STREAM 1
+#endif
+// *d = v (overwrite) or *d += v (accumulate).  STREAM: an evict-first
+// store (st.global.cs) -- the rows are not read back by the kernel.  Used
+// for G <= 8, where a store instruction carries pieces of several rows:
+// C4 batch 177.1 -> 174.0 us, misaligned 1 KiB arrays 474 -> 449, ragged
+// 0-8 KiB 221 -> 211; with one row per warp (G = 32, 16 KiB segments) it
+// cost 5 % (151.5 -> 159.0), so plain stores there.
+template <bool STREAM>
+__device__ __forceinline__ void put_count(unsigned long long *d, unsigned long long v, bool ow) {
+  if (ow) {
+    if (STREAM)
+      __stcs(d, v);
+    else
+      *d = v;
+  } else {
+    *d += v;
+  }
+}
+
 // Row s of out <- the counts lane r of the segment's G-lane group holds
 // (frame bits G*f + r and 32 + G*f + r), rotated by rot = 8*(p0 mod 8) and
 // folded mod w exactly like flush_fw (accumulate.py:115-130).  All G lanes of
@@ -132,6 +153,7 @@ __device__ __forceinline__ void write_row(const SegArgs &a, unsigned long long s
                                           uintptr_t p0, const GroupCounter<G, SM> &c,
                                           uint32_t lane) {
   constexpr int S = 32 / G;
+  constexpr bool kStream = PP_ROW_STREAM && G <= 8;
   const int w = a.width;
   const int r = (int)(lane % G);
   const int rot = (int)(8u * (uint32_t)(p0 & 7u));
@@ -142,8 +164,8 @@ __device__ __forceinline__ void write_row(const SegArgs &a, unsigned long long s
     for (int f = 0; f < S; ++f) {
       const int pe = G * f + r;
       unsigned long long *de = row + ((pe - rot) & 63), *dd = row + ((pe + 32 - rot) & 63);
-      *de = ow ? c.e(f) : *de + c.e(f);
-      *dd = ow ? c.o(f) : *dd + c.o(f);
+      put_count<kStream>(de, c.e(f), ow);
+      put_count<kStream>(dd, c.o(f), ow);
     }
   } else if (G <= w) {
     // lane r's positions G*f + r fall in w/G classes mod w; class of f is f % nc
@@ -156,7 +178,7 @@ __device__ __forceinline__ void write_row(const SegArgs &a, unsigned long long s
         for (int f = cc; f < S; ++f)
           if (f % nc == cc) tot += c.e(f) + c.o(f);
         unsigned long long *d = row + ((G * cc + r - rot) & (w - 1));
-        *d = ow ? tot : *d + tot;
+        put_count<kStream>(d, tot, ow);
       }
     }
   } else {
@@ -170,7 +192,7 @@ __device__ __forceinline__ void write_row(const SegArgs &a, unsigned long long s
     for (int m = w; m < G; m <<= 1) tot += __shfl_xor_sync(gmask, tot, m);
     if (r < w) {
       unsigned long long *d = row + ((r - rot) & (w - 1));
-      *d = ow ? tot : *d + tot;
+      put_count<kStream>(d, tot, ow);
     }
   }
 }
