@@ -126,12 +126,15 @@ __device__ __noinline__ uint4 load_edge(uintptr_t va, uintptr_t p0, uintptr_t e,
 #ifndef PP_ROW_STREAM
 #define PP_ROW_STREAM 1
 #endif
+#ifndef PP_ROW_STREAM_MAXG
+#define PP_ROW_STREAM_MAXG 16
+#endif
 // *d = v (overwrite) or *d += v (accumulate).  STREAM: an evict-first
 // store (st.global.cs) -- the rows are not read back by the kernel.  Used
-// for G <= 8, where a store instruction carries pieces of several rows:
-// C4 batch 177.1 -> 174.0 us, misaligned 1 KiB arrays 474 -> 449, ragged
-// 0-8 KiB 221 -> 211; with one row per warp (G = 32, 16 KiB segments) it
-// cost 5 % (151.5 -> 159.0), so plain stores there.
+// for G <= 16, where a store instruction carries pieces of several rows:
+// C4 batch 177.1 -> 173.5 us, misaligned 1 KiB arrays 473 -> 449, ragged
+// 0-8 KiB 221 -> 210, misaligned 8 KiB 191 -> 185; with one row per warp
+// (G = 32, 16 KiB segments) it measured up to 5 % slower, so plain stores.
 template <bool STREAM>
 __device__ __forceinline__ void put_count(unsigned long long *d, unsigned long long v, bool ow) {
   if (ow) {
@@ -153,7 +156,7 @@ __device__ __forceinline__ void write_row(const SegArgs &a, unsigned long long s
                                           uintptr_t p0, const GroupCounter<G, SM> &c,
                                           uint32_t lane) {
   constexpr int S = 32 / G;
-  constexpr bool kStream = PP_ROW_STREAM && G <= 8;
+  constexpr bool kStream = PP_ROW_STREAM && G <= PP_ROW_STREAM_MAXG;
   const int w = a.width;
   const int r = (int)(lane % G);
   const int rot = (int)(8u * (uint32_t)(p0 & 7u));

@@ -20,7 +20,7 @@ def t(f, k=10):
     b.record(); torch.cuda.synchronize()
     return a.elapsed_time(b) / k * 1e3
 row = []
-for seg, off in ((4096, 0), (1024, 3), (8, 3), (16384, 0)):
+for seg, off in ((4096, 0), (1024, 3), (8, 3), (16384, 0), (8192, 0), (8192, 3)):
     nseg = min(1 << 20, n // seg)
     row.append(f"fixed{seg}@{off}={t(lambda: _lib.check(lib.pp_count_fixed(buf.data_ptr() + off, seg, nseg, 64, out.data_ptr(), 1, sp))):.1f}")
 rng = np.random.default_rng(1)
