@@ -331,11 +331,29 @@ __device__ __forceinline__ uint32_t frame_shift(const void *a) {
 }
 
 // Streaming 16-byte global load that bypasses L1 allocation.
+// Streamed loads: no L1 allocation, and (PP_LDG_EVICT_FIRST) an L2
+// evict-first cache policy, so bytes streamed once do not displace lines
+// still in use (counter rows, offsets, neighbouring segments' edges): ragged
+// 0-8 KiB CSR 209.9 -> 192.0 us per GiB, misaligned 1 KiB arrays 449 -> 437
+// (profiles/r1_segmented_ablation.md).  The createpolicy is volatile and
+// per load: a pure one let ptxas drop the hint (measured: no gain), the
+// volatile asm alone without the hint gains nothing either.
+#ifndef PP_LDG_EVICT_FIRST
+#define PP_LDG_EVICT_FIRST 1
+#endif
 __device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
   uint4 r;
+#if PP_LDG_EVICT_FIRST
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+#else
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
+#endif
   return r;
 }
 
