@@ -310,7 +310,14 @@ constexpr int kLaneStride = 33;  // fr[pos * 33 + lane]
 #ifndef PP_LANE_UNROLL
 #define PP_LANE_UNROLL 1  // 2 and 4 measured: no gain up to 64 words, -15 % at 1 word
 #endif
-constexpr int kLaneUnroll = PP_LANE_UNROLL;  // vectors loaded per step (<= 7)
+constexpr int kLaneUnroll = PP_LANE_UNROLL;
+// The one-lane kernel keeps L1-cached __ldg: a warp's 32 lanes read 32
+// consecutive segments, strided by the segment size, so L1 sectors are
+// shared between lanes; no-allocate + evict-first loads measured 1.03-1.7x
+// slower (PP_LANE_LDG_STREAM=1, scripts/seg_lane_ab.py).
+#ifndef PP_LANE_LDG_STREAM
+#define PP_LANE_LDG_STREAM 0
+#endif  // vectors loaded per step (<= 7)
 
 template <bool FIXED, bool HYBRID = false, bool PTRS = false>
 __global__ void __launch_bounds__(kLaneThreads)
@@ -390,7 +397,11 @@ __global__ void __launch_bounds__(kLaneThreads)
     auto load_vec = [&](uintptr_t va) -> uint4 {
       uint4 v;
       if (va >= vlo && va + 16 <= vhi) {
+#if PP_LANE_LDG_STREAM
+        v = ldg_stream(reinterpret_cast<const uint4 *>(va));
+#else
         v = __ldg(reinterpret_cast<const uint4 *>(va));
+#endif
         if (va < p0 || va + 16 > e) {  // mask to the segment
           const int lo = va < p0 ? (int)(p0 - va) : 0;
           const int hi = va + 16 > e ? (int)(e - va) : 16;

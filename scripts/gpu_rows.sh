@@ -1,1 +1,1 @@
-for p in 1 2; do python scripts/seg_rows_ab.py shipped; PP_LIB_PATH=scripts/variants/lib_ldg0.so python scripts/seg_rows_ab.py ldg0; done; python scripts/count_ab.py count; PP_LOAD_PATH=ldg python scripts/count_ab.py ldgcount; timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -1
+for p in 1 2; do python scripts/seg_lane_ab.py ldg; PP_LIB_PATH=scripts/variants/lib_lanestream.so python scripts/seg_lane_ab.py stream; done
