@@ -698,7 +698,7 @@ def main_gpu(args):
             t_e2e = tt.item()
         e2e = {"value": round(world * nbytes * nst / t_e2e / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": w * 8,
-               "path": "pospopcnt(pinned host tensor) -> pp_count_host: 32 MiB chunks, "
+               "path": "pospopcnt(pinned host tensor) -> pp_count_host: 64 MiB chunks, "
                        "H2D on a copy stream overlapped with counting",
                "steps": nst}
         del pinned, res

@@ -439,7 +439,10 @@ int pp_readonly_sum(const void *data, size_t nbytes, unsigned long long *sink, v
 // previous chunk and the count of the one before.
 namespace {
 constexpr int kNbuf = 3;
-constexpr size_t kChunk = 32ull << 20;
+#ifndef PP_HOST_CHUNK_MIB
+#define PP_HOST_CHUNK_MIB 64  // H2D pieces: 32 MiB 55.0, 64 MiB 55.2, 128 MiB 55.3 GB/s (link max 55.4; scripts/e2e_ab.py)
+#endif
+constexpr size_t kChunk = (size_t)PP_HOST_CHUNK_MIB << 20;
 
 // Parallel memcpy on a persistent pool; the calling thread works too.
 class CopyPool {
