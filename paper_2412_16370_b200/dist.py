@@ -166,6 +166,11 @@ def pospopcnt_sharded(local_data, width, group=None, counters=None, count_fn=Non
         return out.clone()
     fn = count_fn or _count_cuda
     dev = local_data.device if hasattr(local_data, "device") else torch.device("cpu")
+    if dev.type != "cuda" and dist.is_available() and dist.is_initialized() and \
+            dist.get_backend(group) == "nccl":
+        # host-resident shard (counted through pp_count_host): NCCL reduces
+        # device tensors only
+        dev = torch.device("cuda", torch.cuda.current_device())
     local = torch.zeros(width, dtype=torch.int64, device=dev)
     fn(local_data, width, local)
     if dist.is_available() and dist.is_initialized():

@@ -115,3 +115,33 @@ def test_multi_rejects_bad_targets(cuda):
     assert lib.pp_count_multi(data.data_ptr(), 1024, 8, twice, 2, st) == _lib.PP_OK
     torch.cuda.synchronize()
     assert ctr[:8].tolist() == [2048] * 8
+
+
+def test_sharded_host_shard_over_nccl(cuda, oracle):
+    """pospopcnt_sharded on a host-resident shard with the NCCL backend (one
+    rank): the shard goes through pp_count_host, the counters are reduced
+    as a device tensor."""
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    child = (
+        "import sys, numpy as np, torch, torch.distributed as dist\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "from oracle import oracle as O\n"
+        "from paper_2412_16370_b200.dist import pospopcnt_sharded\n"
+        "torch.cuda.set_device(0)\n"
+        f"dist.init_process_group('nccl', init_method='tcp://127.0.0.1:{port}', rank=0,"
+        " world_size=1, device_id=torch.device('cuda', 0))\n"
+        "host = np.random.default_rng(2).integers(0, 256, (40 << 20) + 8, dtype=np.uint8)\n"
+        "got = pospopcnt_sharded(host.tobytes(), 64)\n"
+        "assert got.is_cuda and [int(x) for x in got.cpu()] == O.hs512(host, 0, host.size, 64)\n"
+        "dist.destroy_process_group()\n"
+        "print('ok')\n")
+    res = subprocess.run([sys.executable, "-c", child], capture_output=True, text=True,
+                         timeout=600)
+    assert res.returncode == 0 and res.stdout.strip().endswith("ok"), res.stdout + res.stderr
