@@ -106,6 +106,10 @@ PP_API int pp_count_sync(const void *data, size_t nbytes, int width,
  * pipelined host->device copies overlapped with counting, result added into
  * HOST counters.  Synchronous.  Replaces the bytes-like path of pospopcnt()
  * (kernels.py:315-333 with data = bytes/bytearray/memoryview; cli.py:82-94).
+ * Resources, per calling host thread and device, allocated on first use and
+ * kept: 3 x 64 MiB device buffers (inputs > 1 MiB), 3 x 64 MiB pinned staging
+ * buffers (pageable inputs >= 32 MiB only), 1 MiB pinned + 1 MiB device for
+ * small inputs.
  */
 PP_API int pp_count_host(const void *host_data, size_t nbytes, int width,
                   unsigned long long *host_counters);
