@@ -561,9 +561,9 @@ struct HostCtx {
     dev = -1;
     cudaSetDevice(cur);
   }
-  cudaError_t ensure(int d) {
+  cudaError_t ensure(int d) {  // the slot of device d (host_ctx): set up once
     if (dev == d) return cudaSuccess;
-    release();
+    release();  // a half-built slot after a failed setup
     cudaError_t e;
     dev = d;
     if ((e = cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking))) return e;
@@ -584,7 +584,10 @@ struct HostCtx {
     return cudaSuccess;
   }
 };
-thread_local HostCtx g_host;
+// Per host thread, one context per device (a thread that alternates devices
+// keeps each device's buffers instead of rebuilding or leaking them).
+constexpr int kCtxDevs = 64;
+thread_local HostCtx g_host[kCtxDevs];
 
 bool host_is_pinned(const void *p) {
   cudaPointerAttributes at;
@@ -612,16 +615,11 @@ struct SyncCtx {
   unsigned long long *dcnt = nullptr, *hcnt = nullptr;
   void *pin = nullptr, *dbuf = nullptr;
   cudaStream_t st = nullptr;
-  cudaError_t ensure(int d) {
+  cudaError_t ensure(int d) {  // the slot of device d (sync_ctx): set up once
     if (dev == d) return cudaSuccess;
-    // a previous device's buffers are left to process exit (small)
-    dcnt = hcnt = nullptr;
-    pin = dbuf = nullptr;
-    st = nullptr;
-    dev = -1;
     cudaError_t e;
-    if ((e = cudaMalloc(&dcnt, 64 * sizeof(unsigned long long)))) return e;
-    if ((e = cudaMallocHost(&hcnt, 64 * sizeof(unsigned long long)))) return e;
+    if (!dcnt && (e = cudaMalloc(&dcnt, 64 * sizeof(unsigned long long)))) return e;
+    if (!hcnt && (e = cudaMallocHost(&hcnt, 64 * sizeof(unsigned long long)))) return e;
     dev = d;
     return cudaSuccess;
   }
@@ -633,12 +631,15 @@ struct SyncCtx {
     return cudaSuccess;
   }
 };
-thread_local SyncCtx g_sync;
+thread_local SyncCtx g_sync[kCtxDevs];
+
+// this thread's contexts of device `dev` (nullptr: device index out of range)
+HostCtx *host_ctx(int dev) { return dev >= 0 && dev < kCtxDevs ? &g_host[dev] : nullptr; }
+SyncCtx *sync_ctx(int dev) { return dev >= 0 && dev < kCtxDevs ? &g_sync[dev] : nullptr; }
 
 // Count nbytes (<= kSmallHost) of host memory through the small-call buffers.
-int count_small_host(const void *host, size_t nbytes, int width, unsigned long long *out,
-                     const pp::DevInfo &di) {
-  SyncCtx &c = g_sync;
+int count_small_host(SyncCtx &c, const void *host, size_t nbytes, int width,
+                     unsigned long long *out, const pp::DevInfo &di) {
   cudaError_t e;
   if ((e = c.ensure_small_host())) return cuda_fail(e, "pp_count_host setup");
   if (nbytes >= (256u << 10))
@@ -674,17 +675,18 @@ int pp_count_sync(const void *data, size_t nbytes, int width, unsigned long long
   if ((rc = current_devinfo(&di))) return rc;
   int dev = 0;
   cudaGetDevice(&dev);
-  cudaError_t e = g_sync.ensure(dev);
+  SyncCtx *c = sync_ctx(dev);
+  if (!c) return fail(PP_EARG, "device %d: at most %d devices per process", dev, kCtxDevs);
+  cudaError_t e = c->ensure(dev);
   if (e != cudaSuccess) return cuda_fail(e, "pp_count_sync setup");
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if ((e = cudaMemsetAsync(g_sync.dcnt, 0, (size_t)width * 8, st)))
+  if ((e = cudaMemsetAsync(c->dcnt, 0, (size_t)width * 8, st)))
     return cuda_fail(e, "cudaMemsetAsync");
-  if ((rc = count_device(data, nbytes, width, g_sync.dcnt, st, di))) return rc;
-  if ((e = cudaMemcpyAsync(g_sync.hcnt, g_sync.dcnt, (size_t)width * 8, cudaMemcpyDeviceToHost,
-                           st)))
+  if ((rc = count_device(data, nbytes, width, c->dcnt, st, di))) return rc;
+  if ((e = cudaMemcpyAsync(c->hcnt, c->dcnt, (size_t)width * 8, cudaMemcpyDeviceToHost, st)))
     return cuda_fail(e, "cudaMemcpyAsync");
   if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "cudaStreamSynchronize");
-  for (int j = 0; j < width; ++j) host_counters[j] += g_sync.hcnt[j];
+  for (int j = 0; j < width; ++j) host_counters[j] += c->hcnt[j];
   return PP_OK;
 }
 
@@ -705,13 +707,16 @@ int pp_count_host(const void *host_data, size_t nbytes, int width,
   int dev = 0;
   cudaGetDevice(&dev);
   cudaError_t e;
+  SyncCtx *sc = sync_ctx(dev);
+  HostCtx *hc = host_ctx(dev);
+  if (!sc || !hc) return fail(PP_EARG, "device %d: at most %d devices per process", dev, kCtxDevs);
   if (nbytes <= kSmallHost) {
-    if ((e = g_sync.ensure(dev))) return cuda_fail(e, "pp_count_host setup");
-    return count_small_host(host_data, nbytes, width, host_counters, di);
+    if ((e = sc->ensure(dev))) return cuda_fail(e, "pp_count_host setup");
+    return count_small_host(*sc, host_data, nbytes, width, host_counters, di);
   }
-  e = g_host.ensure(dev);
+  e = hc->ensure(dev);
   if (e != cudaSuccess) return cuda_fail(e, "pp_count_host setup");
-  HostCtx &h = g_host;
+  HostCtx &h = *hc;
   // pageable sources of >= 32 MiB go through our pinned ring + parallel copy
   // pool; below that the driver's own pageable path is as fast (both are
   // host-memcpy-bound at 7-26 GB/s for 1-32 MiB: scripts/host_path_ab.py)
