@@ -798,12 +798,18 @@ static unsigned long long pdl_max_body() {
 // by the stream's unique id, so a recycled handle cannot alias a live
 // stream); launches on one stream are ordered, so a slot is never shared by
 // two running grids.  Captured launches (a graph may be replayed on several
-// streams at once) and streams beyond kSchedSlots use the static order.
+// streams at once) use the static order; a stream beyond kSchedSlots takes
+// over a slot whose last launch has completed (sched_commit), else static.
 // PP_STATIC_SCHED=1 forces the static order (A/B runs).
 constexpr int kSchedSlots = kSchedSlotsAlloc;
 constexpr unsigned long long kDynMinChunks = 4096;  // 128 MiB of 32 KiB chunks
-static unsigned int *&last_slot_next() {  // guarded by sched_lock()
-  static unsigned int *p = nullptr;
+struct SchedSlot {
+  int idx;
+  unsigned int next;      // the counter's value once every launch so far is done
+  cudaEvent_t done;       // recorded after each launch (sched_commit); nullptr: none yet
+};
+static SchedSlot *&last_slot() {  // guarded by sched_lock()
+  static SchedSlot *p = nullptr;
   return p;
 }
 
@@ -815,6 +821,7 @@ std::unique_lock<std::mutex> sched_lock() {
 unsigned int *sched_slot(const DevInfo &di, cudaStream_t st, unsigned long long units,
                          unsigned int *base) {
   static const bool off = std::getenv("PP_STATIC_SCHED") != nullptr;
+  last_slot() = nullptr;
   if (off || !di.sched) return nullptr;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   unsigned long long id = 0;
@@ -823,29 +830,63 @@ unsigned int *sched_slot(const DevInfo &di, cudaStream_t st, unsigned long long 
     cudaGetLastError();
     return nullptr;
   }
-  struct Slot {
-    int idx;
-    unsigned int next;  // the counter's value once every launch so far is done
-  };
-  static std::map<std::pair<unsigned int *, unsigned long long>, Slot> slots;
+  static std::map<std::pair<unsigned int *, unsigned long long>, SchedSlot> slots;
   static std::map<unsigned int *, int> used;
   const auto key = std::make_pair(di.sched, id);
   auto it = slots.find(key);
   if (it == slots.end()) {
     int &n = used[di.sched];
-    if (n >= kSchedSlots) return nullptr;
-    it = slots.emplace(key, Slot{n++, 0u}).first;
+    if (n < kSchedSlots) {
+      it = slots.emplace(key, SchedSlot{n++, 0u, nullptr}).first;
+    } else {
+      // every slot of this device is taken: reuse one whose stream has no
+      // launch in flight any more (its last launch's event has completed),
+      // so a service that keeps creating streams does not fall back to the
+      // static order for good.  The slot's counter continues from `next`.
+      for (auto j = slots.begin(); j != slots.end(); ++j) {
+        if (j->first.first != di.sched) continue;
+        const SchedSlot sl = j->second;
+        if (sl.done) {
+          const cudaError_t q = cudaEventQuery(sl.done);
+          if (q == cudaErrorNotReady) {
+            cudaGetLastError();  // not an error: still running
+            continue;
+          }
+          if (q != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+          }
+        }
+        slots.erase(j);
+        it = slots.emplace(key, sl).first;
+        break;
+      }
+      if (it == slots.end()) return nullptr;  // all busy: static order
+    }
   }
   *base = it->second.next;
   it->second.next += (unsigned int)units;  // mod 2^32, as on the device
-  last_slot_next() = &it->second.next;
+  last_slot() = &it->second;
   return di.sched + it->second.idx;
 }
 
 // A launch that failed to enqueue draws no tickets: give its units back
 // (caller still holds sched_lock(), so this is the slot just handed out).
 void sched_rollback(unsigned long long units) {
-  if (last_slot_next()) *last_slot_next() -= (unsigned int)units;
+  if (last_slot()) last_slot()->next -= (unsigned int)units;
+}
+
+// The launch using the slot just handed out was enqueued on `st`: record
+// its completion event (what a later stream checks before taking the slot).
+void sched_commit(cudaStream_t st) {
+  SchedSlot *sl = last_slot();
+  if (!sl) return;
+  if (!sl->done && cudaEventCreateWithFlags(&sl->done, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    sl->done = nullptr;
+    return;
+  }
+  if (cudaEventRecord(sl->done, st) != cudaSuccess) cudaGetLastError();
 }
 
 template <typename Kern>
@@ -876,7 +917,12 @@ static cudaError_t launch_tma(Kern kernel, unsigned grid, unsigned block, size_t
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, a, sink);
-  if (e != cudaSuccess && a.sched) sched_rollback(a.nchunks);
+  if (a.sched) {
+    if (e != cudaSuccess)
+      sched_rollback(a.nchunks);
+    else
+      sched_commit(st);
+  }
   return e;
 }
 

@@ -91,6 +91,9 @@ unsigned int *sched_slot(const DevInfo &di, cudaStream_t st, unsigned long long 
 std::unique_lock<std::mutex> sched_lock();
 // undo the last sched_slot() hand-out (its launch failed to enqueue)
 void sched_rollback(unsigned long long units);
+// the launch of the last sched_slot() hand-out is enqueued on st: record its
+// completion (a slot is reused by another stream only once that completed)
+void sched_commit(cudaStream_t st);
 
 inline unsigned grid_for(unsigned long long nchunks, unsigned long long cap) {
   const unsigned long long g = nchunks < cap ? nchunks : cap;

@@ -691,7 +691,12 @@ cudaError_t launch_segmented(const SegArgs &a0, const DevInfo &di, cudaStream_t 
     else
       pp_segtma_kernel<32><<<g, kSegTmaThreads, kSegTmaSmem, st>>>(b, ipc);
     const cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess && b.sched) sched_rollback(chunks);
+    if (b.sched) {
+      if (e != cudaSuccess)
+        sched_rollback(chunks);
+      else
+        sched_commit(st);
+    }
     return e;
   }
   const unsigned long long segs_per_block = (kSegThreads / 32) * (32 / G);
@@ -722,7 +727,12 @@ cudaError_t launch_segmented(const SegArgs &a0, const DevInfo &di, cudaStream_t 
     pp_seg_kernel<32><<<g, kSegThreads, 0, st>>>(b);
   }
   const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess && b.sched) sched_rollback(batches);
+  if (b.sched) {
+    if (e != cudaSuccess)
+      sched_rollback(batches);
+    else
+      sched_commit(st);
+  }
   return e;
 }
 

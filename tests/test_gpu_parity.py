@@ -428,3 +428,40 @@ def test_dynamic_schedule_boundaries_and_streams(cuda, oracle):
     assert np.array_equal(got_rows.sum(axis=0), np.array(oracle.hs512(host, 0, 160 << 20, 64),
                                                          dtype=np.uint64))
     assert [int(x) for x in c64.cpu()] == oracle.hs512(host, 0, 160 << 20, 64)
+
+
+def test_scheduler_slots_reused_by_new_streams(cuda, oracle):
+    """More streams than scheduler slots (256 per device): a new stream takes
+    over a slot whose last launch has completed; with every slot busy it
+    falls back to the static order.  Every count must stay exact, including
+    on the old streams afterwards."""
+    torch, pp = cuda
+    from paper_2412_16370_b200 import gen
+    n = 160 << 20  # > 128 MiB: the dynamically scheduled path
+    buf = gen.generate("uniform", n, 0x5107)
+    want = oracle.hs512(buf.cpu().numpy(), 0, n, 8)
+    keep = []
+    for i in range(300):  # sequential: each stream's launch done before the next
+        s = torch.cuda.Stream()
+        c = torch.zeros(8, dtype=torch.int64, device="cuda")
+        with torch.cuda.stream(s):
+            pp.pospopcnt(buf, 8, counters=c)
+        s.synchronize()
+        assert [int(x) for x in c.cpu()] == want, i
+        if i % 50 == 0:
+            keep.append(s)
+    outs = []
+    for i in range(280):  # concurrent: every slot busy for a while
+        s = torch.cuda.Stream()
+        c = torch.zeros(8, dtype=torch.int64, device="cuda")
+        with torch.cuda.stream(s):
+            pp.pospopcnt(buf, 8, counters=c)
+        outs.append((s, c))
+    for s in keep:  # streams whose slots were taken over
+        c = torch.zeros(8, dtype=torch.int64, device="cuda")
+        with torch.cuda.stream(s):
+            pp.pospopcnt(buf, 8, counters=c)
+        outs.append((s, c))
+    torch.cuda.synchronize()
+    for s, c in outs:
+        assert [int(x) for x in c.cpu()] == want
