@@ -209,47 +209,26 @@ def host_threads():
 
 # ------------------------------------------------------------ CPU legs
 
-def time_cpu_port(host_u8, w, min_time, seg=0):
-    """Reference harness methodology (bench.py:124-160): k doubles until a
-    round lasts >= min_time, >= 2 rounds, report the last.  Returns
-    (GB/s, threads, counters of one pass, k, seconds).  seg > 0: the same
-    bytes as seg-byte segments, one counter row each (the segmented config)."""
-    import numpy as np
-    from oracle import oracle as O
-    n = host_u8.size
-    threads = host_threads()
-    if seg:
-        offs = np.arange(n // seg + 1, dtype=np.uint64) * seg
-        one = lambda: O.segments(host_u8, offs, w, threads=threads)  # noqa: E731
-    else:
-        one = lambda: O.hs512(host_u8, 0, n, w, threads=threads)  # noqa: E731
-    once = one()  # warm + result
-    k, rounds = 1, 0
-    while True:
-        t0 = time.perf_counter()
-        for _ in range(k):
-            one()
-        t = time.perf_counter() - t0
-        rounds += 1
-        if rounds >= 2 and t >= min_time:
-            break
-        k = k * 2 if 2 * t < min_time else max(k + 1, int(k * min_time / max(t, 1e-9) * 1.05) + 1)
-    return n * k / t / 1e9, threads, once, k, t
-
-
-def run_reference(args):
-    """--impl reference: the reference's CPU path (oracle port) on host cores."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return 0
-    import numpy as np
-    from oracle import oracle as O
-    cfg = args.config
-    kind, w, nbytes, desc = CONFIGS[cfg]
+def config_dict(cfg, world, per_gpu_bytes, job_bytes, w):
+    """The workload description both arms print (identical dicts, so the
+    driver can match the reference arm's line to this arm's)."""
+    kind, _, _, desc = CONFIGS[cfg]
     if cfg == "c4seg":
-        kind, w, nbytes = "bernoulli", 64, GIB
-    nbytes = min(nbytes, GIB)  # bounded sample of the workload (the metric is a rate)
-    unit_bytes = 1  # bytes of the metric's unit per byte counted
+        par = f"dp{world} (segment ranges; rows stay on their rank, no exchange)"
+    else:
+        par = (f"dp{world} (contiguous 64-byte-cut shards; the {w} counters combined by the "
+               "counting kernel's fused peer exchange, NCCL allreduce fallback)")
+    return {"workload": desc, "word_width": w, "bytes_per_gpu_per_step": per_gpu_bytes,
+            "bytes_per_step_all_gpus": job_bytes,
+            "parallelism": par if world > 1 else "single GPU"}
+
+
+def host_sample(cfg, nbytes):
+    """The config's bytes (same generators and seeds as the GPU arm) for the
+    CPU legs; returns (u8 array, unit_bytes, w, seg)."""
+    from oracle import oracle as O  # bench's cpu_baseline leg: data generation only
+    kind, w, _, _ = CONFIGS[cfg]
+    unit_bytes, seg = 1, 0
     if kind == "uniform":
         host = O.gen_uniform(nbytes, 0xC2 if cfg == "c2" else 0xC1)
     elif kind == "onehot32":
@@ -260,36 +239,110 @@ def run_reference(args):
         host = O.gen_onehot32(nbytes, 0xC3)
         unit_bytes = 4
     elif kind == "bernoulli":
-        host = O.gen_bernoulli(nbytes, 0xC4, 655)
+        host = O.gen_bernoulli(nbytes, 0xC4 + (1 if cfg == "c4seg" else 0), 655)
+        seg = 4096 if cfg == "c4seg" else 0
     else:
         host = O.gen_blocks(nbytes, 0xC5)
-    threads = host_threads()
-    if cfg == "c4seg":  # the same 4 KiB segments, one counter row each
-        offs = np.arange(host.size // 4096 + 1, dtype=np.uint64) * 4096
-        run = lambda: O.segments(host, offs, 64, threads=threads)  # noqa: E731
+    return host, unit_bytes, w, seg
+
+
+def cpu_leg(cfg, sample_bytes, min_time, with_rows=True):
+    """The reference's CPU path on this host: the installed reference's numba
+    kernel on P forked processes (kind "reference"), else the C port on P
+    threads (kind "port").  Returns the cpu_baseline object."""
+    import bench_cpu as BC
+    host, unit_bytes, w, seg = host_sample(cfg, sample_bytes)
+    ref, why = BC.load_reference()
+    info = BC.host_info()
+    what = f"{host.size >> 20} MiB of the {cfg} array" + (
+        " (one-hot u32 words of the codes)" if unit_bytes == 4 else "") + (
+        " as 4 KiB arrays, one reference call each" if seg else "")
+    if ref is not None:
+        # calibrate: steps so one timed run lasts >= min_time
+        k, t = 2, 0.0
+        for _ in range(4):  # k grows until one timed run lasts >= min_time
+            t, _, procs = BC.run_ref_pcore(host, w, k, 1, seg=seg)
+            if t >= min_time:
+                break
+            k = max(k + 1, int(k * min_time / max(t, 1e-6) * 1.1) + 1)
+        gbs = host.size / unit_bytes * k / t / 1e9
+        out = {"value": round(gbs, 3), "unit": "GB/s", "cores": procs, "kind": "reference",
+               "sample": f"{what}, {k} passes in {t:.2f} s on {procs} forked processes: the "
+                         "unmodified reference (baseline/_ref) pospopcnt(InputView, w, "
+                         "kernel='numba') (kernels.py:315-333, 218-270) over contiguous "
+                         "64-byte-cut shards",
+               "host": info}
+        if with_rows:
+            rows = BC.ref_rows(host[: min(host.size, 256 << 20)], w, min_time=min(2.0, min_time),
+                               scalar=cfg in ("c1", "c2"))
+            rows["ref-numba-Pcore"] = {"GBs": out["value"], "cores": procs}
+            out["rows"] = rows
+            out["one_core"] = rows.get("ref-numba-1core", {}).get("GBs")
+        return out
+    gbs, threads, _, k, t = BC.port_pcore(host, w, min_time, seg=seg)
+    gbs /= unit_bytes
+    return {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+            "sample": f"{what}, counted {k}x in {t:.1f} s (last of >=2 rounds); C restatement "
+                      f"of NumbaKernel.run (kernels.py:242-270, oracle/) on {threads} host "
+                      f"threads -- the reference itself is unavailable: {why}",
+            "host": info}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path on the host cores, same
+    config, metric and unit as the GPU arm; rank 0 only under torchrun."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import bench_cpu as BC
+    cfg = args.config
+    kind, w, nbytes, desc = CONFIGS[cfg]
+    world = args.gpus or int(os.environ.get("WORLD_SIZE", "1"))
+    per_gpu = nbytes if cfg not in STRONG else nbytes // world
+    job = per_gpu * world if cfg not in STRONG else nbytes
+    sample = min(nbytes, GIB)  # bounded sample of the workload (the metric is a rate)
+    host, unit_bytes, w, seg = host_sample(cfg, sample)
+    ref, why = BC.load_reference()
+    if ref is not None:
+        t, _, procs = BC.run_ref_pcore(host, w, args.steps, args.warmup, seg=seg)
+        impl_kind = "reference"
+        impl_desc = ("the unmodified reference (baseline/_ref) pospopcnt(InputView, w, "
+                     "kernel='numba') (kernels.py:315-333, 218-270) on "
+                     f"{procs} forked processes over contiguous 64-byte-cut shards")
     else:
-        run = lambda: O.hs512(host, 0, host.size, w, threads=threads)  # noqa: E731
-    for _ in range(args.warmup):
-        run()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        run()
-    t = time.perf_counter() - t0
+        import numpy as np
+        from oracle import oracle as O
+        procs = BC.host_threads()
+        if seg:
+            offs = np.arange(host.size // seg + 1, dtype=np.uint64) * seg
+            run = lambda: O.segments(host, offs, w, threads=procs)  # noqa: E731
+        else:
+            run = lambda: O.hs512(host, 0, host.size, w, threads=procs)  # noqa: E731
+        for _ in range(args.warmup):
+            run()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            run()
+        t = time.perf_counter() - t0
+        impl_kind = "port"
+        impl_desc = (f"C restatement of NumbaKernel.run (kernels.py:242-270, oracle/) on {procs} "
+                     f"threads; the reference itself is unavailable: {why}")
     value = host.size / unit_bytes * args.steps / t / 1e9
     line = {
         "impl": "reference",
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8" if w == 8 else f"u{w}",
-        "data": "synthetic (seeded splitmix64 generators, oracle/pospopcnt_oracle.c)",
-        "config": {"workload": desc, "word_width": w, "bytes_per_step": int(host.size)},
-        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads,
-                         "kind": "port",
-                         "sample": f"whole {host.size >> 20} MiB {cfg} array per step"
-                                   + (" (one-hot u32 words of the codes)" if unit_bytes == 4
-                                      else "") + "; C restatement of NumbaKernel.run "
-                                   f"(kernels.py:242-270) on {threads} threads"},
+        "scaling": "strong" if cfg in STRONG else "weak", "vs_baseline": None,
+        "dtype": "u8" if w == 8 else f"u{w}",
+        "data": "synthetic: seeded splitmix64 generators (the GPU arm's bytes)",
+        "config": config_dict(cfg, world, per_gpu, job, w),
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": procs,
+                         "kind": impl_kind,
+                         "sample": f"a {host.size >> 20} MiB sample of the {cfg} workload per "
+                                   "step" + (" (one-hot u32 words of the codes)"
+                                             if unit_bytes == 4 else "") + "; " + impl_desc,
+                         "host": BC.host_info()},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -299,6 +352,102 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------ GPU arm
+
+def sm100_devices():
+    """Ordinals of the visible sm_100 devices."""
+    import torch
+    return [i for i in range(torch.cuda.device_count())
+            if torch.cuda.get_device_capability(i)[0] == 10]
+
+
+def require_devices(n, local=None):
+    """Fail loudly unless n sm_100 devices are visible (and this rank's is one)."""
+    devs = sm100_devices()
+    if len(devs) < n or (local is not None and local not in devs):
+        raise SystemExit(f"bench.py: {n} rank(s) need {n} visible sm_100 GPUs; visible sm_100 "
+                         f"devices: {devs}")
+
+
+def run_strong_c5(args, lib, world, rank, dev, st, use_dist, peers):
+    """C5 (BASELINE.json configs[4]): the 64 GiB w=16 array with p ~ U[0,1]
+    per 1 MiB block, split over the N ranks in contiguous 64-byte-cut shards
+    generated in place; every step counts each rank's shard and combines the
+    16 counters over the ranks (the fused in-kernel exchange when mapped,
+    else an NCCL allreduce per step inside the timed region).  The job total
+    after all steps must equal steps x the reference's own 64 GiB total."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2412_16370_b200 import _lib, gen
+    from paper_2412_16370_b200.dist import shard_range
+    total, w = CONFIGS["c5"][2], 16
+    lo, hi = shard_range(total, world, rank)
+    shard = gen.generate("blocks", hi - lo, 0xC5, device=dev, word_offset=lo // 8)
+    ptr, n = shard.data_ptr(), hi - lo
+    ctr = torch.zeros(64, dtype=torch.int64, device=dev)
+    fused = peers is not None
+    if fused:
+        peers.zero()
+
+    def step():
+        if fused:
+            _lib.check(lib.pp_count_multi(ptr, n, w, peers.targets, len(peers.targets),
+                                          st.cuda_stream))
+        elif use_dist:  # this step's shard counts, reduced, added to the job total
+            ctr.zero_()
+            _lib.check(lib.pp_count(ptr, n, w, ctr.data_ptr(), st.cuda_stream))
+            dist.all_reduce(ctr)
+            glob.add_(ctr)
+        else:
+            _lib.check(lib.pp_count(ptr, n, w, ctr.data_ptr(), st.cuda_stream))
+    glob = torch.zeros(64, dtype=torch.int64, device=dev)
+    warm, steps = 2, max(3, min(args.steps, 10))
+    for _ in range(warm):
+        step()
+    torch.cuda.synchronize()
+    if use_dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gpu_busy()
+    e0.record(st)
+    for _ in range(steps):
+        step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    if use_dist:
+        dist.barrier()
+    t_ms = e0.elapsed_time(e1)
+    if use_dist:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = tt.item()
+    if fused:
+        peers.sync()
+        res = peers.local
+    elif use_dist:
+        res = glob
+    else:
+        res = ctr
+    got = res.cpu().numpy().view(np.uint64)[:w]
+    want = golden_total("c5_w16_64gib_total")
+    k = warm + steps
+    exact = None if want is None else bool(all(int(g) == k * x for g, x in zip(got, want)))
+    if fused:
+        peers.zero()
+    del shard
+    torch.cuda.empty_cache()
+    gbs = total * steps / (t_ms / 1e3) / 1e9
+    return {"value": round(gbs, 1), "unit": "GB/s", "ms_per_step": round(t_ms / steps, 4),
+            "steps": steps, "warmup": warm, "n_gpus": world, "scaling": "strong",
+            "bytes_total": total, "bytes_per_gpu": n,
+            "exchange": ("fused in-kernel peer adds" if fused else
+                         "NCCL allreduce per step" if use_dist else "none (one GPU)"),
+            "hbm_frac_per_gpu": round(gbs / world / load_peaks()[0], 4),
+            "exact": exact,
+            "exact_reference": "steps x the reference numba total of the 64 GiB array "
+                               "(tests/golden/golden.json c5_w16_64gib_total)"}
+
 
 def main_gpu(args):
     import numpy as np
@@ -311,8 +460,13 @@ def main_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus is not None and args.gpus != world:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one "
+                         "rank per GPU (torchrun --nproc-per-node N, or plain --gpus N)")
     # PP_BENCH_DEVICE / PP_BENCH_BACKEND: test hooks that run N ranks on one
     # GPU over gloo (tests/test_gpu_bench_dist.py); never set for a measurement
+    if "PP_BENCH_DEVICE" not in os.environ:
+        require_devices(world, local)
     local = int(os.environ.get("PP_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -753,27 +907,46 @@ def main_gpu(args):
                "steps": nst}
         del pinned, rows_host, dev_in, rows_dev
 
+    # e2e fanned out over every visible GPU (one host link each) through the
+    # same public call: pospopcnt(pinned host tensor, w, devices="all")
+    e2e_fanout = None
+    if args.e2e and world == 1 and seg_out is None and not categorical:
+        ndev = torch.cuda.device_count()
+        if ndev > 1:
+            pinned = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+            pinned.copy_(buf[offset:offset + nbytes])
+            devs = list(range(ndev))
+            pp.pospopcnt(pinned, w, devices=devs)
+            nst = max(2, min(args.steps, 5))
+            t0 = time.perf_counter()
+            for _ in range(nst):
+                res = pp.pospopcnt(pinned, w, devices=devs)
+            t_f = time.perf_counter() - t0
+            e2e_fanout = {"value": round(nbytes * nst / t_f / 1e9, 3), "unit": "GB/s",
+                          "devices": devs, "h2d_bytes_per_step": nbytes,
+                          "d2h_bytes_per_step": w * 8 * ndev, "steps": nst,
+                          "path": "pospopcnt(pinned host tensor, w, devices=all) -> "
+                                  "pp_count_host_multi: one 64-byte-cut range per device, each "
+                                  "through its own staging ring and host link"}
+            del pinned, res
+        else:
+            e2e_fanout = {"skipped": "one GPU visible: the fan-out has a single link "
+                                     "(tests/test_gpu_fanout.py covers its logic)"}
+
     cpu = None
     if args.cpu_baseline and world == 1 and rank == 0:
         sample = min(nbytes, 256 * MIB)
-        if categorical:
-            # the reference counts categories as one-hot u32 words: the same
-            # draws materialised (4 bytes per code), reported per code byte
-            from oracle import oracle as O
-            host = O.gen_onehot32(4 * sample, 0xC3)
-            gbs, threads, _, k, t = time_cpu_port(host, 32, args.cpu_min_time)
-            gbs /= 4
-            what = f"the one-hot u32 words of the first {sample >> 20} Mi codes"
-        else:
-            host = buf[offset:offset + sample].cpu().numpy()
-            gbs, threads, _, k, t = time_cpu_port(host, w, args.cpu_min_time,
-                                                  seg=4096 if seg_out is not None else 0)
-            what = (f"first {sample >> 20} MiB of the same {cfg} array"
-                    + (" as 4 KiB segments" if seg_out is not None else ""))
-        cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-               "sample": f"{what}, counted {k}x in {t:.1f} s (last of >=2 rounds); C "
-                         "restatement of NumbaKernel.run (kernels.py:242-270), contiguous "
-                         f"shards on {threads} host threads"}
+        cpu = cpu_leg(cfg, sample if cfg != "c4" else 64 * MIB, args.cpu_min_time)
+        if cfg == "c4":
+            cpu["sample"] += " (aligned; the GPU arm's view starts at byte offset 3)"
+
+    # C5 strong scaling beside the weak-scaling headline: the fixed 64 GiB
+    # array split over the N ranks, exact against the reference's own total
+    strong = None
+    if args.strong_c5 and cfg == "c2":
+        del buf
+        torch.cuda.empty_cache()
+        strong = run_strong_c5(args, lib, world, rank, dev, st, use_dist, peers)
 
     if rank == 0:
         line = {
@@ -783,17 +956,13 @@ def main_gpu(args):
             "scaling": "strong" if strong else "weak", "vs_baseline": None,
             "dtype": "u8" if w == 8 else f"u{w}",
             "data": "synthetic: seeded splitmix64 generators, generated in place in HBM",
-            "config": {"workload": desc, "word_width": w,
-                       "bytes_per_gpu_per_step": per_step_bytes,
-                       "bytes_per_step_all_gpus": job_bytes,
-                       "parallelism": (f"dp{world} (shards; fused exchange: the counting "
-                                       "kernel adds into every rank's IPC-mapped counters)"
-                                       if fused else
-                                       f"dp{world} (segment ranges; rows stay on their rank, "
-                                       "no exchange)" if seg_out is not None else
-                                       f"dp{world} (shards, NCCL allreduce of {w} counters "
-                                       "per step)") if world > 1 else "single GPU",
-                       "settle": f"{n_settle + 1} untimed launches (>= {SETTLE_MS:.0f} ms) "
+            "config": config_dict(cfg, world, per_step_bytes, job_bytes, w),
+            "exchange": ("none (rows stay on their rank)" if seg_out is not None else
+                         "fused: the counting kernel adds into every rank's IPC-mapped "
+                         "counters (pp_count_multi)" if fused else
+                         f"NCCL allreduce of the {w} counters per step, pipelined on a side "
+                         "stream") if world > 1 else "none (one GPU)",
+            "timing": {"settle": f"{n_settle + 1} untimed launches (>= {SETTLE_MS:.0f} ms) "
                                  "after the warm-up steps, into scratch counters",
                        "l2": "input >> 126 MB L2, no flush needed" if not flush_l2
                              else f"L2 flushed before every step ({L2_FLUSH_BYTES >> 20} MiB "
@@ -808,6 +977,8 @@ def main_gpu(args):
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_fanout": e2e_fanout,
+            "strong_c5": strong,
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
             "exact": exact,
@@ -844,10 +1015,37 @@ def emit(line):
     out.flush()
 
 
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_torchrun(args):
+    """`bench.py --gpus N` outside torchrun: one rank per GPU, as the driver
+    launches it (python -m torch.distributed.run --nnodes=1 --nproc-per-node
+    N --master-addr 127.0.0.1 ...).  The ranks' stdout is the real stdout
+    (the one JSON line of rank 0)."""
+    if "PP_BENCH_DEVICE" not in os.environ:
+        require_devices(args.gpus)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    return subprocess.run(cmd, stdout=out, env=env).returncode
+
+
 def main():
     claim_stdout()
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="GPUs = ranks (default: WORLD_SIZE under torchrun, else 1); outside "
+                         "torchrun N > 1 relaunches under torch.distributed.run")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
@@ -859,11 +1057,17 @@ def main():
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-min-time", type=float, default=5.0)
+    ap.add_argument("--no-strong-c5", dest="strong_c5", action="store_false",
+                    help="skip the C5 strong-scaling object of the c2 line")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus is not None and args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    if args.gpus and args.gpus > 1 and "LOCAL_RANK" not in os.environ:
+        return relaunch_torchrun(args)
     return main_gpu(args)
 
 

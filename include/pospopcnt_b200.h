@@ -115,6 +115,24 @@ PP_API int pp_count_host(const void *host_data, size_t nbytes, int width,
                   unsigned long long *host_counters);
 
 /*
+ * pp_count_host_multi — pp_count_host fanned out over several GPUs, so one
+ * call over a host buffer uses one host link per device instead of one:
+ * [host_data, +nbytes) is cut into ndevices contiguous ranges at multiples
+ * of 64 bytes (word-complete for every width; counts add), range
+ * k is copied to and counted on devices[k] through that device's own pinned
+ * staging ring and copy stream, and the per-device counters are summed on
+ * the host into host_counters.  Synchronous.  A device may be listed more
+ * than once (each listing is its own range and staging context).  Fan-out
+ * calls are serialised process-wide; ndevices <= PP_MAX_FANOUT.
+ * Replaces: the bytes-like path of pospopcnt() (kernels.py:315-333,
+ * cli.py:82-94), like pp_count_host.
+ */
+#define PP_MAX_FANOUT 16
+PP_API int pp_count_host_multi(const void *host_data, size_t nbytes, int width,
+                               unsigned long long *host_counters, const int *devices,
+                               int ndevices);
+
+/*
  * pp_count_segmented — many independent arrays in one launch.
  * Segment s is device bytes [base + seg_off[s], base + seg_off[s+1]);
  * out (DEVICE, nseg*width uint64, row-major) row s receives its counters.
@@ -215,6 +233,16 @@ PP_API int pp_count_categories(const void *codes, size_t ncodes, int code_bytes,
  */
 PP_API int pp_readonly_sum(const void *data, size_t nbytes, unsigned long long *sink,
                     void *stream);
+
+/*
+ * pp_sched_stats — diagnostics of the dynamic chunk scheduler (per-stream
+ * ticket counters of the persistent counting grids): out4 = {slots handed to
+ * streams, slots taken over from streams whose last launch completed,
+ * launches that found every slot busy and used the static order, launches
+ * with a dynamic slot}, summed over devices, since process start.  No
+ * reference counterpart (test/diagnostic only).
+ */
+PP_API int pp_sched_stats(unsigned long long *out4);
 
 /* ---- seeded synthetic inputs, generated in place on the device ----------
  * Benchmark/test infrastructure.  Byte-identical twins

@@ -21,6 +21,7 @@ PP_SEG_ACCUMULATE, PP_SEG_OVERWRITE = 0, 1
 PP_SEG_HYBRID = 1 << 16    # CSR: <= 512 B arrays one lane each, the rest G lanes
 PP_SEG_BATCH_SHIFT = 20    # PP_SEG_BATCH(t): groups per scheduler ticket hint (0 = auto)
 PP_MAX_TARGETS = 16        # pp_count_multi: counter arrays per call
+PP_MAX_FANOUT = 16         # pp_count_host_multi: devices per call
 PP_IPC_HANDLE_BYTES = 72   # pp_ipc_handle: CUDA IPC handle + offset in the allocation
 ABI_VERSION = 1
 
@@ -35,6 +36,8 @@ SIGNATURES = {
     "pp_count": (_int, [_vp, _sz, _int, _vp, _vp]),
     "pp_count_host": (_int, [_vp, _sz, _int, _vp]),
     "pp_count_sync": (_int, [_vp, _sz, _int, _vp, _vp]),
+    "pp_count_host_multi": (_int, [_vp, _sz, _int, _vp, _vp, _int]),
+    "pp_sched_stats": (_int, [_vp]),
     "pp_count_frame": (_int, [_vp, _sz, _vp, _vp]),
     "pp_count_multi": (_int, [_vp, _sz, _int, _vp, _int, _vp]),
     "pp_ipc_handle": (_int, [_vp, _vp]),

@@ -690,17 +690,10 @@ int pp_count_sync(const void *data, size_t nbytes, int width, unsigned long long
   return PP_OK;
 }
 
-int pp_count_host(const void *host_data, size_t nbytes, int width,
-                  unsigned long long *host_counters) {
-  if (!width_ok(width)) return fail(PP_EWIDTH, "word width must be one of (8, 16, 32, 64), got %d", width);
-  if (nbytes % (size_t)(width / 8))
-    return fail(PP_ELENGTH, "%zu bytes is not a multiple of the %d-byte word size", nbytes,
-                width / 8);
-  if (!host_counters) return fail(PP_EARG, "host_counters is NULL");
-  if (nbytes == 0) return PP_OK;
-  if (!host_data) return fail(PP_EARG, "host_data is NULL");
-  if (is_device_memory(host_data) || is_device_memory(host_counters))
-    return fail(PP_EARG, "pp_count_host takes host buffers (device memory: use pp_count)");
+namespace {
+// pp_count_host on the CURRENT device (validated arguments, nbytes > 0).
+int count_host_current(const void *host_data, size_t nbytes, int width,
+                       unsigned long long *host_counters) {
   int rc;
   pp::DevInfo di;
   if ((rc = current_devinfo(&di))) return rc;
@@ -767,6 +760,137 @@ int pp_count_host(const void *host_data, size_t nbytes, int width,
     return cuda_fail(e, "cudaMemcpyAsync D2H");
   if ((e = cudaStreamSynchronize(h.count))) return cuda_fail(e, "cudaStreamSynchronize");
   for (int j = 0; j < width; ++j) host_counters[j] += h.hcnt[j];
+  return PP_OK;
+}
+
+int host_args_check(const void *host_data, size_t nbytes, int width,
+                    const unsigned long long *host_counters) {
+  if (!width_ok(width)) return fail(PP_EWIDTH, "word width must be one of (8, 16, 32, 64), got %d", width);
+  if (nbytes % (size_t)(width / 8))
+    return fail(PP_ELENGTH, "%zu bytes is not a multiple of the %d-byte word size", nbytes,
+                width / 8);
+  if (!host_counters) return fail(PP_EARG, "host_counters is NULL");
+  if (nbytes == 0) return PP_OK;
+  if (!host_data) return fail(PP_EARG, "host_data is NULL");
+  if (is_device_memory(host_data) || is_device_memory(host_counters))
+    return fail(PP_EARG, "pp_count_host takes host buffers (device memory: use pp_count)");
+  return PP_OK;
+}
+
+// Persistent workers of pp_count_host_multi: worker k runs its range on its
+// device with its own (thread-local) staging context, kept across calls.
+// One fan-out call at a time (g_fan_call); a worker serves one job at a time.
+struct FanJob {
+  int dev = 0;
+  const void *src = nullptr;
+  size_t n = 0;
+  int width = 8;
+  unsigned long long out[64] = {};
+  int rc = PP_OK;
+  std::string err;
+};
+class FanWorker {
+ public:
+  FanWorker() : th_([this] { loop(); }) { th_.detach(); }
+  void post(FanJob *j) {
+    std::lock_guard<std::mutex> lk(m_);
+    job_ = j;
+    done_ = false;
+    cv_.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> lk(m_);
+    done_cv_.wait(lk, [&] { return done_; });
+  }
+
+ private:
+  void loop() {
+    for (;;) {
+      FanJob *j;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return job_ != nullptr; });
+        j = job_;
+      }
+      cudaError_t e = cudaSetDevice(j->dev);
+      if (e != cudaSuccess) {
+        j->rc = cuda_fail(e, "cudaSetDevice");
+      } else {
+        std::memset(j->out, 0, sizeof j->out);
+        j->rc = count_host_current(j->src, j->n, j->width, j->out);
+      }
+      if (j->rc) j->err = g_err;
+      std::lock_guard<std::mutex> lk(m_);
+      job_ = nullptr;
+      done_ = true;
+      done_cv_.notify_all();
+    }
+  }
+  std::mutex m_;
+  std::condition_variable cv_, done_cv_;
+  FanJob *job_ = nullptr;
+  bool done_ = true;
+  std::thread th_;
+};
+std::mutex g_fan_call;
+FanWorker &fan_worker(int k) {
+  static FanWorker *w[PP_MAX_FANOUT] = {};
+  static std::mutex m;
+  std::lock_guard<std::mutex> lk(m);
+  if (!w[k]) w[k] = new FanWorker();  // intentionally leaked (process lifetime)
+  return *w[k];
+}
+}  // namespace
+
+int pp_count_host(const void *host_data, size_t nbytes, int width,
+                  unsigned long long *host_counters) {
+  int rc;
+  if ((rc = host_args_check(host_data, nbytes, width, host_counters)) || nbytes == 0) return rc;
+  return count_host_current(host_data, nbytes, width, host_counters);
+}
+
+int pp_count_host_multi(const void *host_data, size_t nbytes, int width,
+                        unsigned long long *host_counters, const int *devices, int ndevices) {
+  int rc;
+  if ((rc = host_args_check(host_data, nbytes, width, host_counters))) return rc;
+  if (!devices || ndevices < 1 || ndevices > PP_MAX_FANOUT)
+    return fail(PP_EARG, "need 1..%d devices, got %d", PP_MAX_FANOUT, ndevices);
+  int ndev_visible = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev_visible);
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) {
+    cudaGetLastError();
+    return fail(PP_ENODEV, "no CUDA device: %s", cudaGetErrorString(e));
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  for (int k = 0; k < ndevices; ++k)
+    if (devices[k] < 0 || devices[k] >= ndev_visible)
+      return fail(PP_EARG, "devices[%d] = %d: %d devices visible", k, devices[k], ndev_visible);
+  if (nbytes == 0) return PP_OK;
+  // contiguous ranges cut at multiples of 64 bytes (word-complete for every
+  // width): their counts add; tiny inputs use fewer devices
+  const size_t units = nbytes / 64;
+  int n = ndevices;
+  if ((size_t)n > units) n = units ? (int)units : 1;
+  std::lock_guard<std::mutex> one_call(g_fan_call);
+  FanJob jobs[PP_MAX_FANOUT];
+  const uint8_t *src = static_cast<const uint8_t *>(host_data);
+  for (int k = 0; k < n; ++k) {
+    const size_t lo = units * k / n * 64;
+    const size_t hi = (k == n - 1) ? nbytes : units * (k + 1) / n * 64;
+    jobs[k].dev = devices[k];
+    jobs[k].src = src + lo;
+    jobs[k].n = hi - lo;
+    jobs[k].width = width;
+    fan_worker(k).post(&jobs[k]);
+  }
+  for (int k = 0; k < n; ++k) fan_worker(k).wait();
+  for (int k = 0; k < n; ++k)
+    if (jobs[k].rc) {
+      g_err = "device " + std::to_string(jobs[k].dev) + ": " + jobs[k].err;
+      return jobs[k].rc;
+    }
+  for (int k = 0; k < n; ++k)
+    for (int j = 0; j < width; ++j) host_counters[j] += jobs[k].out[j];
   return PP_OK;
 }
 

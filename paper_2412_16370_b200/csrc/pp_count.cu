@@ -805,13 +805,22 @@ constexpr int kSchedSlots = kSchedSlotsAlloc;
 constexpr unsigned long long kDynMinChunks = 4096;  // 128 MiB of 32 KiB chunks
 struct SchedSlot {
   int idx;
-  unsigned int next;      // the counter's value once every launch so far is done
-  cudaEvent_t done;       // recorded after each launch (sched_commit); nullptr: none yet
+  unsigned int next;  // the counter's value once every launch so far is done
+  // completion of the slot's last launch (recorded by sched_commit).  It is
+  // created BEFORE the slot's first hand-out, so a slot some launch has used
+  // always has one; nullptr = the slot was never handed out.
+  cudaEvent_t done;
+  // a completion record failed: the slot's in-flight state is unknown, so it
+  // is never taken over by another stream (its own stream may keep it)
+  bool pinned;
 };
 static SchedSlot *&last_slot() {  // guarded by sched_lock()
   static SchedSlot *p = nullptr;
   return p;
 }
+// pp_sched_stats: {slots handed to streams, takeovers, all-busy static
+// launches, dynamic launches}, all devices (guarded by sched_lock())
+static unsigned long long g_sched_stats[4];
 
 std::unique_lock<std::mutex> sched_lock() {
   static std::mutex m;
@@ -823,11 +832,14 @@ unsigned int *sched_slot(const DevInfo &di, cudaStream_t st, unsigned long long 
   static const bool off = std::getenv("PP_STATIC_SCHED") != nullptr;
   last_slot() = nullptr;
   if (off || !di.sched) return nullptr;
+  // an error the caller left pending must survive this function: with one
+  // pending, take the static order and touch no CUDA error state at all
+  if (cudaPeekAtLastError() != cudaSuccess) return nullptr;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   unsigned long long id = 0;
   if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone ||
       cudaStreamGetId(st, &id) != cudaSuccess) {
-    cudaGetLastError();
+    cudaGetLastError();  // ours (nothing was pending)
     return nullptr;
   }
   static std::map<std::pair<unsigned int *, unsigned long long>, SchedSlot> slots;
@@ -837,56 +849,70 @@ unsigned int *sched_slot(const DevInfo &di, cudaStream_t st, unsigned long long 
   if (it == slots.end()) {
     int &n = used[di.sched];
     if (n < kSchedSlots) {
-      it = slots.emplace(key, SchedSlot{n++, 0u, nullptr}).first;
+      it = slots.emplace(key, SchedSlot{n++, 0u, nullptr, false}).first;
+      ++g_sched_stats[0];
     } else {
       // every slot of this device is taken: reuse one whose stream has no
       // launch in flight any more (its last launch's event has completed),
       // so a service that keeps creating streams does not fall back to the
       // static order for good.  The slot's counter continues from `next`.
       for (auto j = slots.begin(); j != slots.end(); ++j) {
-        if (j->first.first != di.sched) continue;
+        if (j->first.first != di.sched || j->second.pinned) continue;
         const SchedSlot sl = j->second;
         if (sl.done) {
           const cudaError_t q = cudaEventQuery(sl.done);
-          if (q == cudaErrorNotReady) {
-            cudaGetLastError();  // not an error: still running
-            continue;
-          }
           if (q != cudaSuccess) {
-            cudaGetLastError();
+            cudaGetLastError();  // NotReady (still running) or a fault: not free
             continue;
           }
         }
         slots.erase(j);
         it = slots.emplace(key, sl).first;
+        ++g_sched_stats[1];
         break;
       }
-      if (it == slots.end()) return nullptr;  // all busy: static order
+      if (it == slots.end()) {  // all busy: static order
+        ++g_sched_stats[2];
+        return nullptr;
+      }
     }
   }
-  *base = it->second.next;
-  it->second.next += (unsigned int)units;  // mod 2^32, as on the device
-  last_slot() = &it->second;
-  return di.sched + it->second.idx;
+  SchedSlot &sl = it->second;
+  if (!sl.done && cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming) != cudaSuccess) {
+    // without a completion event the slot could be taken over while this
+    // launch runs: static order for this launch, retry the event next time
+    cudaGetLastError();
+    sl.done = nullptr;
+    return nullptr;
+  }
+  *base = sl.next;
+  sl.next += (unsigned int)units;  // mod 2^32, as on the device
+  last_slot() = &sl;
+  ++g_sched_stats[3];
+  return di.sched + sl.idx;
 }
 
 // A launch that failed to enqueue draws no tickets: give its units back
 // (caller still holds sched_lock(), so this is the slot just handed out).
 void sched_rollback(unsigned long long units) {
-  if (last_slot()) last_slot()->next -= (unsigned int)units;
+  if (last_slot()) {
+    last_slot()->next -= (unsigned int)units;
+    --g_sched_stats[3];
+  }
 }
 
 // The launch using the slot just handed out was enqueued on `st`: record
 // its completion event (what a later stream checks before taking the slot).
+// The event exists (sched_slot created it before the hand-out); if the
+// record fails the event still shows an older, completed launch, so the
+// slot is pinned to its stream instead.
 void sched_commit(cudaStream_t st) {
   SchedSlot *sl = last_slot();
   if (!sl) return;
-  if (!sl->done && cudaEventCreateWithFlags(&sl->done, cudaEventDisableTiming) != cudaSuccess) {
-    cudaGetLastError();
-    sl->done = nullptr;
-    return;
+  if (!sl->done || cudaEventRecord(sl->done, st) != cudaSuccess) {
+    cudaGetLastError();  // the launch itself succeeded just before: this error is ours
+    sl->pinned = true;
   }
-  if (cudaEventRecord(sl->done, st) != cudaSuccess) cudaGetLastError();
 }
 
 template <typename Kern>
@@ -975,6 +1001,13 @@ cudaError_t launch_readonly(const CountArgs &a, unsigned long long *sink, const 
 }
 
 }  // namespace pp
+
+extern "C" __attribute__((visibility("default"))) int pp_sched_stats(unsigned long long *out4) {
+  if (!out4) return 4;  // PP_EARG
+  auto lk = pp::sched_lock();
+  for (int i = 0; i < 4; ++i) out4[i] = pp::g_sched_stats[i];
+  return 0;
+}
 
 #if PP_TIMELINE
 extern "C" __attribute__((visibility("default"))) int pp_debug_timeline(unsigned long long *out) {

@@ -650,6 +650,10 @@ cudaError_t launch_segmented(const SegArgs &a0, const DevInfo &di, cudaStream_t 
   if ((a.lanes_per_segment == 2 || a.lanes_per_segment == 4) && !seg_use_tma(a, di, &ipc))
     a.lanes_per_segment = a.lanes_per_segment == 2 ? 1 : 8;
   const int G = a.lanes_per_segment;
+  // G = 1 (asked for, or G = 2 demoted above) counts every segment one lane
+  // each: the hybrid split must not survive, or the one-lane kernel would
+  // count only the short segments and no pass would take the long ones
+  if (G == 1) a.short_max = 0;
   if (a.short_max && G != 1) {
     // hybrid: short segments one lane each, then the rest with G lanes
     SegArgs sh = a;

@@ -45,28 +45,46 @@ def shard_range(total_bytes, world, rank, align=SHARD_ALIGN):
 
 
 class PeerCounters:
-    """Every rank's 64 counters, mapped into this process (CUDA IPC).
+    """Every rank's counter arrays, mapped into this process (CUDA IPC).
 
     Collective constructor: every rank of ``group`` must create one (on its
-    own device).  ``local`` is this rank's int64[64] counter tensor; after
-    every rank has run ``count`` over its shard and ``sync()`` has returned,
-    ``local`` holds the sum over all ranks' shards.
+    own device).  Each rank owns ``NGEN`` int64[64] counter arrays in one
+    allocation; the IPC handle of that allocation is exchanged once.
+
+    * generation 0 (``local``) is the raw accumulate-only mode: after every
+      rank has run ``count`` over its shard and ``sync()`` has returned,
+      ``local`` holds the sum over all ranks' shards, cumulative until
+      ``zero()``;
+    * generations 1 and 2 serve ``count_call`` (and so
+      ``pospopcnt_sharded(peers=...)``): call i counts into generation
+      1 + i % 2 of every rank, a barrier waits for every rank's remote adds,
+      then each rank reads its own array and zeroes it.  A rank can be at
+      most one call ahead of a slower peer (it must pass the next call's
+      barrier, which the peer reaches only after its read-and-zero), and
+      that call targets the other generation -- so no remote add of a later
+      call can land in an array before it is read, and every call returns
+      exactly its own job total (the reference's accumulate contract,
+      core.py:82-87, SPEC.md:64-69).
     """
+
+    NGEN = 3
 
     def __init__(self, group=None, device=None):
         self.lib = _lib.load()
         self.group = group
         self.device = torch.device(device) if device is not None else \
             torch.device("cuda", torch.cuda.current_device())
-        self.local = torch.zeros(W_MAX, dtype=torch.int64, device=self.device)
+        self.gens = torch.zeros((self.NGEN, W_MAX), dtype=torch.int64, device=self.device)
+        self.local = self.gens[0]
+        self.calls = 0
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         if self.world > _lib.PP_MAX_TARGETS:
             raise ValueError(f"at most {_lib.PP_MAX_TARGETS} ranks per fused exchange")
         handle = ctypes.create_string_buffer(_lib.PP_IPC_HANDLE_BYTES)
         with torch.cuda.device(self.device):
-            _lib.check(self.lib.pp_ipc_handle(self.local.data_ptr(), handle))
-        self.handle = handle.raw  # IPC handle of the allocation + offset of `local` in it
+            _lib.check(self.lib.pp_ipc_handle(self.gens.data_ptr(), handle))
+        self.handle = handle.raw  # IPC handle of the allocation + offset of `gens` in it
         handles = [handle.raw]
         if self.world > 1:
             handles = [None] * self.world
@@ -78,7 +96,7 @@ class PeerCounters:
             try:
                 for r, h in enumerate(handles):
                     if r == self.rank:
-                        ptrs.append(self.local.data_ptr())
+                        ptrs.append(self.gens.data_ptr())
                         continue
                     p = ctypes.c_void_p()
                     _lib.check(self.lib.pp_ipc_open(ctypes.create_string_buffer(h, len(h)),
@@ -98,17 +116,38 @@ class PeerCounters:
             raise RuntimeError(f"fused exchange unavailable (no peer mapping): {err}") from err
         # own array first: it is the kernel's primary target
         ptrs.insert(0, ptrs.pop(self.rank))
-        self.targets = (ctypes.c_void_p * len(ptrs))(*ptrs)
+        row = W_MAX * 8
+        self.gen_targets = [(ctypes.c_void_p * len(ptrs))(*[p + g * row for p in ptrs])
+                            for g in range(self.NGEN)]
+        self.targets = self.gen_targets[0]
         self.sync()
 
-    def count(self, data, nbytes, width, stream=None):
-        """Count device bytes [data, data+nbytes) into every rank's counters."""
+    def count(self, data, nbytes, width, stream=None, gen=0):
+        """Count device bytes [data, data+nbytes) into generation ``gen`` of
+        every rank's counters (raw mode: no synchronisation)."""
         st = torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream
-        _lib.check(self.lib.pp_count_multi(ctypes.c_void_p(data), nbytes, width, self.targets,
-                                           len(self.targets), ctypes.c_void_p(st)))
+        tg = self.gen_targets[gen]
+        _lib.check(self.lib.pp_count_multi(ctypes.c_void_p(data), nbytes, width, tg,
+                                           len(tg), ctypes.c_void_p(st)))
+
+    def count_call(self, data, nbytes, width):
+        """Collective: this call's job total (int64[width], on this rank's
+        device) of every rank's shard -- exactly this call's, whatever ran
+        before (see the class docstring for the generation protocol)."""
+        g = 1 + self.calls % 2
+        self.calls += 1
+        self.count(data, nbytes, width, gen=g)
+        self.sync()  # every rank's remote adds into generation g are complete
+        row = self.gens[g]
+        out = row[:width].clone()
+        row.zero_()
+        # the zero must be complete before this rank enters the next call's
+        # barrier: peers may add into generation g again one call after that
+        torch.cuda.synchronize(self.device)
+        return out
 
     def zero(self):
-        """Reset the job counters (collective: all ranks, before counting)."""
+        """Reset the raw-mode counters (collective: all ranks, before counting)."""
         self.local.zero_()
         self.sync()
 
@@ -140,7 +179,8 @@ def pospopcnt_sharded(local_data, width, group=None, counters=None, count_fn=Non
 
     With ``peers`` (a ``PeerCounters``) the combine is fused into the
     counting kernel (remote atomics into every rank's counters over NVLink)
-    and only a barrier follows; ``peers.local`` accumulates across calls.
+    and only a barrier follows; every call returns (or adds) exactly its own
+    job total, like the NCCL path.
     Otherwise the shard is counted into a fresh tensor and all-reduced over
     the group (NCCL, or gloo for CPU tensors).  ``count_fn(data, width,
     counters_tensor)`` replaces the per-shard counter in that path; it exists
@@ -157,13 +197,11 @@ def pospopcnt_sharded(local_data, width, group=None, counters=None, count_fn=Non
         view = InputView.of(local_data).check_complete(width)
         if not view.on_device:
             raise ValueError("the fused exchange needs the shard in device memory")
-        peers.count(view.base.data_ptr() + view.offset, view.nbytes, width)
-        peers.sync()
-        out = peers.local[:width]
+        out = peers.count_call(view.base.data_ptr() + view.offset, view.nbytes, width)
         if counters is not None:
             counters[:width] += out.to(counters.device, counters.dtype)
             return counters
-        return out.clone()
+        return out
     fn = count_fn or _count_cuda
     dev = local_data.device if hasattr(local_data, "device") else torch.device("cpu")
     if dev.type != "cuda" and dist.is_available() and dist.is_initialized() and \

@@ -40,6 +40,29 @@ from .core import (
 )
 
 KERNEL_ENV = "POSPOPCNT_KERNEL"
+# host inputs fanned out over several GPUs (pp_count_host_multi): "all" or a
+# comma-separated list of CUDA device ordinals; unset = the current device
+DEVICES_ENV = "POSPOPCNT_B200_DEVICES"
+
+
+def _resolve_devices(devices):
+    """None | "all" | "0,1,..." | iterable of ints -> tuple of ordinals, or None."""
+    if devices is None:
+        devices = os.environ.get(DEVICES_ENV) or None
+        if devices is None:
+            return None
+    if isinstance(devices, str):
+        if devices.strip().lower() == "all":
+            import torch
+            n = torch.cuda.device_count()
+            if n < 1:
+                raise KernelUnavailableError("no CUDA device is visible")
+            return tuple(range(n))
+        devices = [int(x) for x in devices.split(",") if x.strip()]
+    devs = tuple(int(d) for d in devices)
+    if not 1 <= len(devs) <= _lib.PP_MAX_FANOUT:
+        raise ValueError(f"devices: 1..{_lib.PP_MAX_FANOUT} CUDA device ordinals, got {devs!r}")
+    return devs
 
 
 @dataclass(frozen=True)
@@ -127,9 +150,14 @@ class B200Kernel:
     name = "b200"
     r = 128
 
-    def __init__(self):
+    def __init__(self, devices=None):
+        """``devices``: host-resident inputs are split over these GPUs, one
+        host link each (pp_count_host_multi); "all", a list of ordinals, or
+        None (``POSPOPCNT_B200_DEVICES``, else the current device).  Device
+        inputs are always counted where they live."""
         self.descriptor = KernelDescriptor(self.name, self.r, 2 * self.r)
         self._avail = None
+        self.devices = devices
 
     def __repr__(self):
         return f"<kernel {self.name} r={self.r}>"
@@ -197,7 +225,12 @@ class B200Kernel:
         dev_idx = None
         if is_torch_tensor(counters) and counters.is_cuda:
             dev_idx = counters.device.index
-        if dev_idx is not None:
+        devs = _resolve_devices(self.devices)
+        if devs is not None and (len(devs) > 1 or dev_idx is None):
+            arr = (ctypes.c_int * len(devs))(*devs)
+            _lib.check(lib.pp_count_host_multi(ptr, view.nbytes, w, out.ctypes.data, arr,
+                                               len(devs)))
+        elif dev_idx is not None:
             import torch
             with torch.cuda.device(dev_idx):
                 _lib.check(lib.pp_count_host(ptr, view.nbytes, w, out.ctypes.data))
@@ -254,7 +287,7 @@ def select_kernel(override=None):
     return best
 
 
-def pospopcnt(data, width, counters=None, kernel=None):
+def pospopcnt(data, width, counters=None, kernel=None, *, devices=None):
     """Add the positional population count of ``data`` to ``counters``.
 
     Same contract as the reference (kernels.py:315-333): ``data`` is
@@ -262,7 +295,13 @@ def pospopcnt(data, width, counters=None, kernel=None):
     InputView over any of these; its length must be a multiple of width/8.
     Returns the counter object (a fresh list when ``counters`` is None).
     ``kernel`` may be a kernel object, a kernel name, or None.
+    ``devices`` (keyword only, an extension): split a HOST input over these
+    GPUs ("all" or a list of ordinals), one host link each.
     """
+    if devices is not None:
+        if kernel is not None and not (isinstance(kernel, str) and kernel == "b200"):
+            raise ValueError("devices= applies to the b200 kernel only")
+        kernel = B200Kernel(devices=devices)
     check_width(width)
     view = InputView.of(data).check_complete(width)
     if counters is None:

@@ -56,6 +56,18 @@ def test_error_codes_without_device():
     assert lib.pp_count_segmented(buf.ctypes.data, None, 3, 8, cnt.ctypes.data, 0, None) == \
         _lib.PP_EARG
     assert lib.pp_gen_bernoulli(buf.ctypes.data, 64, 1, 0, 70000, None) == _lib.PP_EARG
+    devs = (ctypes.c_int * 2)(0, 0)
+    assert lib.pp_count_host_multi(buf.ctypes.data, 64, 12, cnt.ctypes.data, devs, 2) == \
+        _lib.PP_EWIDTH
+    assert lib.pp_count_host_multi(buf.ctypes.data, 3, 16, cnt.ctypes.data, devs, 2) == \
+        _lib.PP_ELENGTH
+    assert lib.pp_count_host_multi(buf.ctypes.data, 64, 16, cnt.ctypes.data, None, 2) == \
+        _lib.PP_EARG
+    assert lib.pp_count_host_multi(buf.ctypes.data, 64, 16, cnt.ctypes.data, devs, 0) == \
+        _lib.PP_EARG
+    stats = np.zeros(4, dtype=np.uint64)
+    assert lib.pp_sched_stats(stats.ctypes.data) == _lib.PP_OK
+    assert lib.pp_sched_stats(None) == _lib.PP_EARG
     for code in range(6):
         assert lib.pp_strerror(code)
     assert (cnt == 0).all()

@@ -335,3 +335,21 @@ def test_segment_plan_shape():
     assert (p.lanes, p.hybrid) == (32, True)
     assert plan(np.full(1000, 256)).lanes == 1
     assert plan(np.full(10, 4096)).order.numel() == 10
+
+
+def test_devices_argument_parsing(monkeypatch):
+    """pospopcnt(..., devices=) / B200Kernel(devices=) / POSPOPCNT_B200_DEVICES:
+    host inputs fanned out over several GPUs (pp_count_host_multi)."""
+    from paper_2412_16370_b200 import kernels as K
+    monkeypatch.delenv(K.DEVICES_ENV, raising=False)
+    assert K._resolve_devices(None) is None
+    assert K._resolve_devices([0, 0, 1]) == (0, 0, 1)
+    assert K._resolve_devices("1, 2") == (1, 2)
+    monkeypatch.setenv(K.DEVICES_ENV, "0,3")
+    assert K._resolve_devices(None) == (0, 3)
+    with pytest.raises(ValueError):
+        K._resolve_devices([])
+    with pytest.raises(ValueError):
+        K._resolve_devices([0] * 17)
+    with pytest.raises(ValueError):  # another kernel cannot take devices=
+        K.pospopcnt(b"\x00" * 8, 8, kernel=object(), devices=[0])

@@ -36,7 +36,14 @@ def test_bench_line_contract(cuda):
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["peak"] > 0
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
     c = d["cpu_baseline"]
-    assert c["kind"] == "port" and c["cores"] >= 1 and c["value"] > 0 and c["sample"]
+    assert c["kind"] in ("reference", "port") and c["cores"] >= 1 and c["value"] > 0
+    assert c["sample"] and c["host"]["cpu_model"]
+    if c["kind"] == "reference":  # baseline/_ref shipped: BASELINE.md section 3 rows
+        assert {"ref-numba-1core", "ref-numba-Pcore", "ref-default", "ref-scalar"} <= \
+            set(c["rows"])
+        assert c["one_core"] > 0 and c["rows"]["ref-default"]["kernel"] == "numpy"
+    s = d["strong_c5"]
+    assert s["exact"] is True and s["bytes_total"] == 64 << 30 and s["value"] > 1000
     e = d["e2e"]
     assert e["unit"] == "GB/s" and e["value"] > 0
     assert e["h2d_bytes_per_step"] == d["config"]["bytes_per_gpu_per_step"]
@@ -48,6 +55,10 @@ def test_bench_line_contract(cuda):
 
 def test_reference_arm_contract():
     d = _run("--impl", "reference", "--steps", "1", "--warmup", "3")
+    g = _run("--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu-baseline",
+             "--no-strong-c5")
+    # same workload description as the GPU arm: the driver matches the lines
+    assert d["config"] == g["config"] and d["metric"] == g["metric"]
     assert d["impl"] == "reference" and d["unit"] == "GB/s" and d["value"] > 0
     assert d["cpu_baseline"]["value"] == d["value"] and d["e2e"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["gpu_launches"] == 0

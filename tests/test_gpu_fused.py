@@ -56,10 +56,12 @@ def _worker(rank, world, port, total, lead, width, seed):
     try:
         got = pospopcnt_sharded(full[lo:hi], width, peers=peers)
         assert [int(x) for x in got.cpu()] == want, (rank, width)
-        # peers.local accumulates across calls; counters= adds into a tensor
+        # every call returns exactly its own job total; counters= adds it
         acc = torch.ones(width, dtype=torch.int64, device="cuda")
         pospopcnt_sharded(full[lo:hi], width, peers=peers, counters=acc)
-        assert [int(x) for x in acc.cpu()] == [2 * v + 1 for v in want], (rank, width)
+        assert [int(x) for x in acc.cpu()] == [v + 1 for v in want], (rank, width)
+        got = pospopcnt_sharded(full[lo:hi], width, peers=peers)
+        assert [int(x) for x in got.cpu()] == want, (rank, width)
         # reset and count a second, uneven split: ranks' kernels race freely
         peers.zero()
         cut = [0, total // 3 // 8 * 8, total]
@@ -93,6 +95,49 @@ def _worker(rank, world, port, total, lead, width, seed):
 def test_fused_exchange_one_gpu(cuda, world, width, total, lead):
     mp.spawn(_worker, args=(world, _free_port(), total, lead, width, 0xF5ED + width),
              nprocs=world, join=True)
+
+
+def _calls_worker(rank, world, port, ncalls, seed):
+    """ncalls back-to-back sharded calls over tiny, uneven shards, nothing
+    zeroed in between: ranks race through the calls at different speeds
+    (rank r sleeps r-dependent amounts), and every call must return exactly
+    that call's job total (dist.PeerCounters generation protocol)."""
+    import sys
+    import time
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    import numpy as np
+    from oracle import oracle as O
+    from paper_2412_16370_b200.dist import PeerCounters, pospopcnt_sharded
+
+    rng = np.random.default_rng(seed)
+    peers = PeerCounters(device="cuda:0")
+    try:
+        for i in range(ncalls):
+            width = (8, 16, 32, 64)[i % 4]
+            # the same per-call data on every rank (seeded by the call index)
+            host = np.random.default_rng(seed + i).integers(0, 256, 4096 + 64 * (i % 7),
+                                                             dtype=np.uint8)
+            want = O.hs512(host, 0, host.size, width)
+            cut = (host.size // world) // 8 * 8
+            lo, hi = rank * cut, (host.size if rank == world - 1 else (rank + 1) * cut)
+            shard = torch.from_numpy(host[lo:hi].copy()).cuda()
+            if rng.random() < 0.3:
+                time.sleep(0.002 * (rank + 1))
+            got = pospopcnt_sharded(shard, width, peers=peers)
+            assert [int(x) for x in got.cpu()] == want, (rank, i, width)
+    finally:
+        dist.barrier()
+        peers.close()
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_exchange_per_call_totals(cuda, world):
+    mp.spawn(_calls_worker, args=(world, _free_port(), 200, 0xCA11), nprocs=world, join=True)
 
 
 def test_multi_rejects_bad_targets(cuda):

@@ -430,19 +430,44 @@ def test_dynamic_schedule_boundaries_and_streams(cuda, oracle):
     assert [int(x) for x in c64.cpu()] == oracle.hs512(host, 0, 160 << 20, 64)
 
 
+def _raw_streams(n):
+    """n fresh CUDA streams (cudaStreamCreateWithFlags through cuda-python):
+    torch.cuda.Stream() recycles a pool of 32 per device, which never gets
+    past the scheduler's 256 slots."""
+    import torch
+    from cuda.bindings import runtime as rt
+    out = []
+    for _ in range(n):
+        err, h = rt.cudaStreamCreateWithFlags(rt.cudaStreamNonBlocking)
+        assert err == rt.cudaError_t.cudaSuccess, err
+        out.append((int(h), torch.cuda.ExternalStream(int(h))))
+    return out
+
+
+def _sched_stats():
+    import ctypes
+    from paper_2412_16370_b200 import _lib
+    out = (ctypes.c_uint64 * 4)()
+    assert _lib.load().pp_sched_stats(out) == 0
+    return list(out)  # handed out, taken over, all-busy static, dynamic launches
+
+
 def test_scheduler_slots_reused_by_new_streams(cuda, oracle):
     """More streams than scheduler slots (256 per device): a new stream takes
     over a slot whose last launch has completed; with every slot busy it
-    falls back to the static order.  Every count must stay exact, including
-    on the old streams afterwards."""
+    falls back to the static order.  Real streams (not torch's pool of 32),
+    and pp_sched_stats proves both paths ran.  Every count must stay exact,
+    including on the old streams afterwards."""
     torch, pp = cuda
+    from cuda.bindings import runtime as rt
     from paper_2412_16370_b200 import gen
     n = 160 << 20  # > 128 MiB: the dynamically scheduled path
     buf = gen.generate("uniform", n, 0x5107)
     want = oracle.hs512(buf.cpu().numpy(), 0, n, 8)
+    s0 = _sched_stats()
+    streams = _raw_streams(300)
     keep = []
-    for i in range(300):  # sequential: each stream's launch done before the next
-        s = torch.cuda.Stream()
+    for i, (h, s) in enumerate(streams):  # sequential: each launch done before the next
         c = torch.zeros(8, dtype=torch.int64, device="cuda")
         with torch.cuda.stream(s):
             pp.pospopcnt(buf, 8, counters=c)
@@ -450,13 +475,28 @@ def test_scheduler_slots_reused_by_new_streams(cuda, oracle):
         assert [int(x) for x in c.cpu()] == want, i
         if i % 50 == 0:
             keep.append(s)
+    s1 = _sched_stats()
+    # the first 256 - (slots used before) streams got fresh slots, the rest
+    # took over completed ones
+    assert s1[1] - s0[1] >= 300 - 256, (s0, s1)
+    busy = _raw_streams(300)
+    # every stream waits on one host-released gate: all their launches are
+    # in flight at once, so every slot is busy and the later ones must take
+    # the static order
+    gate = torch.cuda.Event()
+    blocker = torch.cuda.Stream()
+    with torch.cuda.stream(blocker):
+        torch.cuda._sleep(int(2e9))  # ~1 s of device time
+        gate.record(blocker)
     outs = []
-    for i in range(280):  # concurrent: every slot busy for a while
-        s = torch.cuda.Stream()
+    for h, s in busy:
         c = torch.zeros(8, dtype=torch.int64, device="cuda")
+        s.wait_event(gate)
         with torch.cuda.stream(s):
             pp.pospopcnt(buf, 8, counters=c)
         outs.append((s, c))
+    s2 = _sched_stats()
+    assert s2[2] > s1[2], (s1, s2)  # all-busy launches used the static order
     for s in keep:  # streams whose slots were taken over
         c = torch.zeros(8, dtype=torch.int64, device="cuda")
         with torch.cuda.stream(s):
@@ -465,3 +505,5 @@ def test_scheduler_slots_reused_by_new_streams(cuda, oracle):
     torch.cuda.synchronize()
     for s, c in outs:
         assert [int(x) for x in c.cpu()] == want
+    for h, _ in streams + busy:
+        rt.cudaStreamDestroy(h)

@@ -77,7 +77,7 @@ def test_c1_exhaustive_sweep_via_segments(cuda, oracle):
                 dig["sha256_u64_rows"], w
 
 
-@pytest.mark.parametrize("lanes", (None, 1, 8, 16, 32))
+@pytest.mark.parametrize("lanes", (None, 1, 2, 4, 8, 16, 32))
 def test_ragged_random_segments_poison(cuda, oracle, rng, lanes):
     torch, pp = cuda
     for w in (8, 16, 32, 64):
@@ -93,7 +93,10 @@ def test_ragged_random_segments_poison(cuda, oracle, rng, lanes):
         out = pp.pospopcnt_segmented(view, offs, w, lanes=lanes)
         want = oracle.segments(host, (offs + base).astype(np.uint64), w)
         assert np.array_equal(out.cpu().numpy().view(np.uint64), want), w
-        if lanes in (None, 8):  # the hybrid split over the same mixed lengths
+        # the hybrid split over the same mixed lengths, with every lane hint:
+        # G = 2 demotes to one lane per segment on CSR offsets, which must
+        # drop the split (rows of long segments were never written)
+        if True:
             hy = pp.pospopcnt_segmented(view, offs, w, lanes=lanes, hybrid=True)
             assert np.array_equal(hy.cpu().numpy().view(np.uint64), want), w
         # accumulate semantics
