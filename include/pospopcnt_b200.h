@@ -244,6 +244,26 @@ PP_API int pp_readonly_sum(const void *data, size_t nbytes, unsigned long long *
  */
 PP_API int pp_sched_stats(unsigned long long *out4);
 
+/*
+ * pp_check_status — memory-safety evidence (no compute-sanitizer needed).
+ * A checked build of this library (PP_CHECK_BOUNDS=1:
+ * libpospopcnt_b200_checked.so, build.build_checked()) tests every global
+ * load / bulk-copy source range against the caller's [data, data+nbytes)
+ * before issuing it, every shared-memory stage index, every chunk id, and
+ * per launch that the chunks consumed total exactly the chunks issued; a
+ * failed check skips the access and is recorded.  out6 = {1 if this is a
+ * checked build, failed checks, source line of the first, its address, its
+ * allowed [lo, hi)}; reset != 0 clears the record.  Unchecked builds report
+ * {0, 0, ...}.  Reference contract: edges.py:1-10, no byte outside the
+ * buffer is read (pkg/tests/test_kernels.py:83-91).
+ */
+PP_API int pp_check_status(unsigned long long *out6, int reset);
+/* pp_debug_corrupt — checked builds only: corrupt the launchers' derived
+ * ranges (1: body runs 32 bytes past the end, 2: head/tail edge bytes
+ * outside, 3: fixed segmented base 16 bytes low) so a test can show the
+ * checks fire; 0 restores normal launches.  PP_EARG in unchecked builds. */
+PP_API int pp_debug_corrupt(int mode);
+
 /* ---- seeded synthetic inputs, generated in place on the device ----------
  * Benchmark/test infrastructure.  Byte-identical twins
  * live in oracle/pospopcnt_oracle.c.  word_offset lets a shard generate its

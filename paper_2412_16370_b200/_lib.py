@@ -38,6 +38,8 @@ SIGNATURES = {
     "pp_count_sync": (_int, [_vp, _sz, _int, _vp, _vp]),
     "pp_count_host_multi": (_int, [_vp, _sz, _int, _vp, _vp, _int]),
     "pp_sched_stats": (_int, [_vp]),
+    "pp_check_status": (_int, [_vp, _int]),
+    "pp_debug_corrupt": (_int, [_int]),
     "pp_count_frame": (_int, [_vp, _sz, _vp, _vp]),
     "pp_count_multi": (_int, [_vp, _sz, _int, _vp, _int, _vp]),
     "pp_ipc_handle": (_int, [_vp, _vp]),
@@ -91,7 +93,31 @@ def load():
             _load_error = f"libpospopcnt_b200.so unavailable: {exc}"
             raise KernelUnavailableError(_load_error) from exc
         _lib = lib
+        if os.environ.get("PP_CHECK_REPORT"):
+            import atexit
+            atexit.register(_check_report, os.environ["PP_CHECK_REPORT"])
         return _lib
+
+
+def check_status(reset=False):
+    """pp_check_status as a dict (checked builds: PP_CHECK_BOUNDS=1)."""
+    out = (ctypes.c_uint64 * 6)()
+    check(load().pp_check_status(out, 1 if reset else 0))
+    return {"checked_build": bool(out[0]), "fails": int(out[1]), "first_line": int(out[2]),
+            "first_addr": int(out[3]), "first_lo": int(out[4]), "first_hi": int(out[5])}
+
+
+def _check_report(path):
+    """PP_CHECK_REPORT=<file>: at exit, append this process's check record
+    (the tests running a checked build collect one line per process)."""
+    try:
+        st = check_status()
+        with open(path, "a") as f:
+            f.write(f"{os.getpid()} {int(st['checked_build'])} {st['fails']} {st['first_line']} "
+                    f"{st['first_addr']:#x} {st['first_lo']:#x} {st['first_hi']:#x}\n")
+    except Exception as exc:  # noqa: BLE001 - reported as a failed record
+        with open(path, "a") as f:
+            f.write(f"{os.getpid()} error {exc!r}\n")
 
 
 def check(rc):

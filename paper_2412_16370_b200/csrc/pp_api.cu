@@ -19,6 +19,7 @@
 namespace {
 
 thread_local std::string g_err;
+std::atomic<int> g_corrupt{0};  // pp_debug_corrupt (checked builds only)
 
 int fail(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
 int fail(int code, const char *fmt, ...) {
@@ -119,9 +120,48 @@ int count_device(const void *data, size_t nbytes, int width, unsigned long long 
 
 }  // namespace
 
+namespace pp {
+int chk_corrupt_mode() { return g_corrupt.load(std::memory_order_relaxed); }
+}  // namespace pp
+
 extern "C" {
 
 int pp_abi_version(void) { return PP_ABI_VERSION; }
+
+int pp_check_status(unsigned long long *out6, int reset) {
+  if (!out6) return fail(PP_EARG, "out6 is NULL");
+  std::memset(out6, 0, 6 * sizeof *out6);
+#if PP_CHECK_BOUNDS
+  out6[0] = 1;
+  pp::ChkRecHost r[2];
+  cudaError_t e;
+  if ((e = pp::chk_read_count(&r[0], reset != 0))) return cuda_fail(e, "pp_check_status");
+  if ((e = pp::chk_read_seg(&r[1], reset != 0))) return cuda_fail(e, "pp_check_status");
+  for (const auto &x : r) {
+    if (x.fails && !out6[1]) {
+      out6[2] = x.first_line;
+      out6[3] = x.first_addr;
+      out6[4] = x.first_lo;
+      out6[5] = x.first_hi;
+    }
+    out6[1] += x.fails;
+  }
+#else
+  (void)reset;
+#endif
+  return PP_OK;
+}
+
+int pp_debug_corrupt(int mode) {
+#if PP_CHECK_BOUNDS
+  if (mode < 0 || mode > 3) return fail(PP_EARG, "corruption mode %d not in 0..3", mode);
+  g_corrupt.store(mode);
+  return PP_OK;
+#else
+  (void)mode;
+  return fail(PP_EARG, "pp_debug_corrupt exists in checked builds only (PP_CHECK_BOUNDS=1)");
+#endif
+}
 
 const char *pp_strerror(int code) {
   switch (code) {
@@ -409,6 +449,8 @@ int pp_count_fixed(const void *base, size_t seg_bytes, size_t nseg, int width,
   a.batch_groups = seg_batch_hint(flags);
   a.lanes_per_segment =
       seg_lanes(flags, seg_bytes, ((uintptr_t)base % 16 == 0) && (seg_bytes % 16 == 0));
+  a.chk_lo = (uintptr_t)base;  // the caller's range (checked builds)
+  a.chk_hi = (uintptr_t)base + (uintptr_t)(seg_bytes * nseg);
   return seg_common(a, stream);
 }
 

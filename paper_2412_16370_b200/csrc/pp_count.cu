@@ -79,7 +79,8 @@ constexpr unsigned long long kLdgChunkBytes = kLdgChunkVecs * 16ull;
 // warp 0 of CTA 0.  Lane l < 16 takes head byte l, lane 16+l tail byte l.
 __device__ __forceinline__ void count_edges(Counter &c, const uint8_t *head, uint32_t hb,
                                             const uint8_t *tail, uint32_t tb, uint32_t lane,
-                                            const TC &t) {
+                                            const TC &t, uintptr_t chk_lo = 0,
+                                            uintptr_t chk_hi = 0) {
   const uint8_t *p = nullptr;
   if (lane < 16) {
     if (lane < hb) p = head + lane;
@@ -88,7 +89,7 @@ __device__ __forceinline__ void count_edges(Counter &c, const uint8_t *head, uin
   }
   unsigned long long fw = 0;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // input complete (PDL)
-  if (p) fw = (unsigned long long)__ldg(p) << frame_shift(p);
+  if (p && PP_CHK_RANGE(p, 1, chk_lo, chk_hi)) fw = (unsigned long long)__ldg(p) << frame_shift(p);
   c.ce += wcount((uint32_t)fw, t);
   c.co += wcount((uint32_t)(fw >> 32), t);
 }
@@ -449,6 +450,7 @@ __device__ __forceinline__ uint64_t edge_load(const CountArgs &a, uint32_t lane)
     p = a.tail + unit * (lane - 16);
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");  // input complete (PDL)
+  if (p && !PP_CHK_RANGE(p, unit, a.chk_lo, a.chk_hi)) p = nullptr;
   if (CB == 0) return p ? (uint64_t)__ldg(p) << frame_shift(p) : 0ull;
   if (!p) return 0xFFFFFFFFull;
   return CB == 1 ? __ldg(p)
@@ -541,8 +543,13 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         const unsigned long long off = ch * Sh::kStageBytes;
         const unsigned long long rem = a.body_bytes - off;
         const uint32_t bytes = (uint32_t)(rem < Sh::kStageBytes ? rem : Sh::kStageBytes);
-        mbar_arrive_expect_tx(&full[stage], bytes);
-        bulk_g2s(stages + stage * Sh::kStageVecs, a.body + off, bytes, &full[stage], pol);
+        if (PP_CHK(stage < (uint32_t)Sh::kStages) &&
+            PP_CHK_RANGE(a.body + off, bytes, a.chk_lo, a.chk_hi)) {
+          mbar_arrive_expect_tx(&full[stage], bytes);
+          bulk_g2s(stages + stage * Sh::kStageVecs, a.body + off, bytes, &full[stage], pol);
+        } else {  // checked build, failed check: no copy, the stage completes empty
+          mbar_arrive(&full[stage]);
+        }
         ch = a.sched ? gridDim.x + (unsigned long long)(atomicAdd(a.sched, 1u) - a.sched_base)
                      : ch + gridDim.x;
         if (++stage == Sh::kStages) {
@@ -566,10 +573,21 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     if (kCount && blockIdx.x == 0 && warp == 0) edge = edge_load<kEdgeCB>(a, lane);
     uint32_t stage = 0, phase = 0;
     const uint32_t tid = threadIdx.x;
+#if PP_CHECK_BOUNDS
+    unsigned long long prev_ch = 0, seen = 0;
+#endif
     for (bool first = true;; first = false) {
       mbar_wait(&full[stage], phase);
       const unsigned long long ch = chunk_id[stage];
       if (ch == kNoChunk) break;
+#if PP_CHECK_BOUNDS
+      // chunk ids: in range, strictly increasing per CTA (static stride and
+      // scheduler tickets both increase); a skipped or repeated ring phase
+      // shows up here or in the grid-wide total below
+      PP_CHK(ch < nchunks && (first || ch > prev_ch));
+      prev_ch = ch;
+      ++seen;
+#endif
       if (first && threadIdx.x == 0) PP_TL(2);
       const uint4 *sv = stages + stage * Sh::kStageVecs;
       uint4 v[8];
@@ -577,6 +595,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       const unsigned long long off = ch * Sh::kStageBytes;
       const unsigned long long rem = a.body_bytes - off;
       if (rem >= Sh::kStageBytes) {
+        PP_CHK(stage < (uint32_t)Sh::kStages && tid + 7 * (NCW * 32) < (uint32_t)Sh::kStageVecs);
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = sv[tid + i * (NCW * 32)];
       } else {
@@ -623,6 +642,16 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         phase ^= 1;
       }
     }
+#if PP_CHECK_BOUNDS
+    if (threadIdx.x == 0 && a.chk_ctr) {  // this CTA's chunks, then the grid-wide total
+      atomicAdd(a.chk_ctr, seen);
+      __threadfence();
+      if (atomicAdd(a.chk_ctr + 1, 1ull) == gridDim.x - 1ull) {
+        const unsigned long long tot = atomicAdd(a.chk_ctr, 0ull);
+        if (tot != nchunks) chk_fail(__LINE__, tot, nchunks, nchunks);
+      }
+    }
+#endif
     if (kCount) {
       if (threadIdx.x == 0) PP_TL(4);
       c.finish(t);
@@ -669,19 +698,24 @@ __global__ void __launch_bounds__(kLdgThreads)
     uint4 v[8];
     if ((ch + 1) * kLdgChunkVecs <= nvec) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = ldg_stream(body + base + i * kLdgThreads);
+      for (int i = 0; i < 8; ++i)
+        v[i] = PP_CHK_RANGE(body + base + i * kLdgThreads, 16, a.chk_lo, a.chk_hi)
+                   ? ldg_stream(body + base + i * kLdgThreads)
+                   : make_uint4(0u, 0u, 0u, 0u);
     } else {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const unsigned long long idx = base + i * kLdgThreads;
-        v[i] = idx < nvec ? ldg_stream(body + idx) : make_uint4(0u, 0u, 0u, 0u);
+        v[i] = idx < nvec && PP_CHK_RANGE(body + idx, 16, a.chk_lo, a.chk_hi)
+                   ? ldg_stream(body + idx)
+                   : make_uint4(0u, 0u, 0u, 0u);
       }
     }
     c.eat8(v, t);
   }
   c.finish(t);
   if (blockIdx.x == 0 && warp == 0)
-    count_edges(c, a.head, a.head_bytes, a.tail, a.tail_bytes, lane, t);
+    count_edges(c, a.head, a.head_bytes, a.tail, a.tail_bytes, lane, t, a.chk_lo, a.chk_hi);
   atomicAdd(&frame[lane], c.ce);
   atomicAdd(&frame[32 + lane], c.co);
   __syncthreads();
@@ -702,6 +736,8 @@ void split_range(const uint8_t *data, unsigned long long nbytes,
   a->tail = data + hb + body;
   a->tail_bytes = (uint32_t)(nbytes - hb - body);
   a->rot = (int)(8u * ((uintptr_t)data & 7u));
+  a->chk_lo = (uintptr_t)data;  // the caller's range, before any corruption (checked builds)
+  a->chk_hi = (uintptr_t)data + nbytes;
 }
 
 unsigned long long codes8_chunk_bytes() { return CatShape::kStageBytes; }
@@ -932,6 +968,17 @@ static cudaError_t launch_tma(Kern kernel, unsigned grid, unsigned block, size_t
     lk = sched_lock();
     a.sched = sched_slot(di, st, a.nchunks, &a.sched_base);
   }
+#if PP_CHECK_BOUNDS
+  // per-launch {chunks consumed, CTAs finished} (stream-ordered scratch)
+  if (cudaMallocAsync(reinterpret_cast<void **>(&a.chk_ctr), 16, st) != cudaSuccess ||
+      cudaMemsetAsync(a.chk_ctr, 0, 16, st) != cudaSuccess)
+    return cudaGetLastError();
+  switch (chk_corrupt_mode()) {  // pp_debug_corrupt: derived fields go wrong
+    case 1: a.body_bytes += 32; break;                       // bulk copy past the end
+    case 2: a.head -= 1; a.head_bytes += 1; a.tail_bytes += 1; break;  // edge bytes outside
+    default: break;
+  }
+#endif
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
@@ -943,6 +990,9 @@ static cudaError_t launch_tma(Kern kernel, unsigned grid, unsigned block, size_t
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, a, sink);
+#if PP_CHECK_BOUNDS
+  cudaFreeAsync(a.chk_ctr, st);
+#endif
   if (a.sched) {
     if (e != cudaSuccess)
       sched_rollback(a.nchunks);
@@ -998,6 +1048,23 @@ cudaError_t launch_readonly(const CountArgs &a, unsigned long long *sink, const 
   const unsigned g = grid_for(a.nchunks, (unsigned long long)di.count_sms);
   return launch_tma(pp_tma_kernel<0>, g, kTmaThreads, kTmaSmemBytes, st, a, sink,
                     a.body_bytes < pdl_max_body(), di);
+}
+
+cudaError_t chk_read_count(ChkRecHost *out, bool reset) {
+#if PP_CHECK_BOUNDS
+  ChkRec r{};
+  cudaError_t e = cudaMemcpyFromSymbol(&r, pp_chk, sizeof r);
+  if (e != cudaSuccess) return e;
+  *out = ChkRecHost{r.fails, r.first_line, r.first_addr, r.first_lo, r.first_hi};
+  if (reset) {
+    const ChkRec z{};
+    return cudaMemcpyToSymbol(pp_chk, &z, sizeof z);
+  }
+#else
+  (void)reset;
+  *out = ChkRecHost{};
+#endif
+  return cudaSuccess;
 }
 
 }  // namespace pp

@@ -22,6 +22,52 @@ namespace pp {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// ---- checked builds (PP_CHECK_BOUNDS=1; build.build_checked()) -------------
+// The reference's contract is that no byte outside the caller's buffer is
+// read (edges.py:1-10, pkg/tests/test_kernels.py:83-91).  A checked build
+// tests, before it happens, every global load and bulk-copy source range
+// against the caller's range (CountArgs/SegArgs chk_lo/chk_hi, set by the
+// host API from the caller's own pointer and length before any split), every
+// shared-memory stage index, every chunk id a consumer sees (in range and,
+// per CTA, strictly increasing) and, at the end of each counting grid, that
+// the chunks consumed add up to exactly the chunks of the launch (a skipped
+// or repeated mbarrier phase breaks that).  A failed check skips the access
+// (nothing out of range is ever touched) and is recorded in this translation
+// unit's ChkRec, read back by pp_check_status().  No __trap(): a recorded
+// failure leaves the context usable.  Unchecked builds compile all of it out.
+#ifndef PP_CHECK_BOUNDS
+#define PP_CHECK_BOUNDS 0
+#endif
+struct ChkRec {
+  unsigned int fails;       // failed checks since the last reset
+  unsigned int first_line;  // source line of the first one
+  unsigned long long first_addr, first_lo, first_hi;  // its address and allowed range
+};
+#if PP_CHECK_BOUNDS
+static __device__ ChkRec pp_chk;  // one per translation unit (no -rdc)
+static __device__ __noinline__ void chk_fail(int line, unsigned long long addr, unsigned long long lo,
+                                      unsigned long long hi) {
+  if (atomicAdd(&pp_chk.fails, 1u) == 0u) {
+    pp_chk.first_line = (unsigned)line;
+    pp_chk.first_addr = addr;
+    pp_chk.first_lo = lo;
+    pp_chk.first_hi = hi;
+  }
+}
+#define PP_CHK_RANGE(p, n, lo, hi) \
+  ::pp::chk_range(reinterpret_cast<uintptr_t>(p), (unsigned long long)(n), (lo), (hi), __LINE__)
+#define PP_CHK(cond) ((cond) ? true : (::pp::chk_fail(__LINE__, 0ull, 0ull, 0ull), false))
+static __device__ __forceinline__ bool chk_range(uintptr_t a, unsigned long long n, uintptr_t lo,
+                                          uintptr_t hi, int line) {
+  if (a >= lo && a + n >= a && a + n <= hi) return true;
+  chk_fail(line, a, lo, hi);
+  return false;
+}
+#else
+#define PP_CHK_RANGE(p, n, lo, hi) true
+#define PP_CHK(cond) true
+#endif
+
 __device__ __forceinline__ uint32_t xor3(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
   asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(a), "r"(b), "r"(c));

@@ -32,6 +32,10 @@ struct CountArgs {
   // slots exhausted)
   unsigned int *sched;
   unsigned int sched_base;
+  // checked builds (PP_CHECK_BOUNDS): the caller's byte range as the API
+  // received it, and a per-launch {chunks consumed, CTAs finished} pair
+  uintptr_t chk_lo, chk_hi;
+  unsigned long long *chk_ctr;
 };
 
 struct SegArgs {
@@ -58,7 +62,22 @@ struct SegArgs {
   // processing order of the G-lane kernel (pp_count_segmented_order): slot k
   // counts segment order[k]; nullptr = slot k is segment k
   const unsigned int *order;
+  // checked builds: the caller's byte range (fixed segments: [base, base +
+  // nseg * seg_bytes)); 0/0 = derived in the kernel (CSR: [base + seg_off[0],
+  // base + seg_off[nseg]); pointer mode: each array's own range)
+  uintptr_t chk_lo, chk_hi;
 };
+
+// checked builds: this translation unit's failure record (read / reset)
+struct ChkRecHost {
+  unsigned int fails, first_line;
+  unsigned long long first_addr, first_lo, first_hi;
+};
+cudaError_t chk_read_count(ChkRecHost *out, bool reset);
+cudaError_t chk_read_seg(ChkRecHost *out, bool reset);
+// checked builds: deliberate argument corruption (pp_debug_corrupt), applied
+// by the launchers after the caller's range was recorded; 0 = none
+int chk_corrupt_mode();
 
 enum class LoadPath : int { kTma = 0, kLdg = 1 };
 

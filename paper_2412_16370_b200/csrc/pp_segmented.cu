@@ -45,12 +45,13 @@ static unsigned long long seg_batches(unsigned long long nseg, int G, unsigned T
 // Bytes [max(va, lo), min(va + 16, hi)) of the aligned 16-byte block at va,
 // zero elsewhere: the masked head / tail vector of a segment.  Exact-bounds
 // byte loads, so nothing outside the segment is ever read.
-__device__ __noinline__ uint4 load_partial(uintptr_t va, uintptr_t lo, uintptr_t hi) {
+__device__ __noinline__ uint4 load_partial(uintptr_t va, uintptr_t lo, uintptr_t hi,
+                                           uintptr_t chk_lo = 0, uintptr_t chk_hi = 0) {
   uint32_t q[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
   for (int b = 0; b < 16; ++b) {
     const uintptr_t ad = va + b;
-    if (ad >= lo && ad < hi)
+    if (ad >= lo && ad < hi && PP_CHK_RANGE(ad, 1, chk_lo, chk_hi))
       q[b >> 2] |= (uint32_t)__ldg(reinterpret_cast<const uint8_t *>(ad)) << (8 * (b & 3));
   }
   return make_uint4(q[0], q[1], q[2], q[3]);
@@ -109,8 +110,10 @@ __device__ __forceinline__ uint32_t byte_range_mask(int q, int lo, int hi) {
 // inside the caller's view (they then belong to neighbouring segments),
 // one vector load and a byte mask; else exact-bounds byte loads.
 __device__ __noinline__ uint4 load_edge(uintptr_t va, uintptr_t p0, uintptr_t e,
-                                           uintptr_t view_lo, uintptr_t view_hi) {
+                                           uintptr_t view_lo, uintptr_t view_hi,
+                                           uintptr_t chk_lo = 0, uintptr_t chk_hi = 0) {
   if (va >= view_lo && va + 16 <= view_hi) {
+    if (!PP_CHK_RANGE(va, 16, chk_lo, chk_hi)) return make_uint4(0u, 0u, 0u, 0u);
     uint4 v = __ldg(reinterpret_cast<const uint4 *>(va));
     const int lo = va < p0 ? (int)(p0 - va) : 0;
     const int hi = va + 16 > e ? (int)(e - va) : 16;
@@ -120,7 +123,7 @@ __device__ __noinline__ uint4 load_edge(uintptr_t va, uintptr_t p0, uintptr_t e,
     v.w &= byte_range_mask(3, lo, hi);
     return v;
   }
-  return load_partial(va, p0, e);
+  return load_partial(va, p0, e, chk_lo, chk_hi);
 }
 
 #ifndef PP_ROW_STREAM
@@ -219,6 +222,10 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
   const uintptr_t view_lo = a.ptrs ? 0 : base_u + (a.seg_off ? a.seg_off[0] : 0ull);
   const uintptr_t view_hi =
       a.ptrs ? 0 : base_u + (a.seg_off ? a.seg_off[a.nseg] : a.nseg * a.seg_bytes);
+  // checked builds: the caller's range (host-given for fixed segments,
+  // else this view; pointer mode: per array, below)
+  const uintptr_t chk_lo = a.chk_hi ? a.chk_lo : view_lo;
+  const uintptr_t chk_hi = a.chk_hi ? a.chk_hi : view_hi;
   // group gw first, then (a.sched) tickets of the stream's scheduler slot,
   // one per group of S segments (group nw + ticket), else the grid stride:
   // ragged lengths no longer leave a few warps with most of the bytes
@@ -251,11 +258,18 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
       const unsigned long long kf0 = g.hp ? 1 : 0;
       const unsigned long long kf1 = (g.tp && g.nvv) ? g.nvv - 1 : g.nvv;
       const uint4 *vp = reinterpret_cast<const uint4 *>(g.A) + r;
+      // checked builds: whole vectors must lie inside the segment itself,
+      // edge vectors inside the caller's range
+      const uintptr_t clo = a.ptrs ? g.p0 : chk_lo, chi = a.ptrs ? g.e : chk_hi;
       auto load_round = [&](unsigned long long k0, uint4 (&v)[8]) {
         if (k0 + r >= kf0 && k0 + r + 7 * G < kf1) {
           // fast path: 8 full vectors, base pointer + immediate offsets
 #pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = ldg_stream(vp + k0 + j * G);
+          for (int j = 0; j < 8; ++j)
+            v[j] = PP_CHK_RANGE(vp + k0 + j * G, 16, g.p0, g.e) &&
+                           PP_CHK_RANGE(vp + k0 + j * G, 16, clo, chi)
+                       ? ldg_stream(vp + k0 + j * G)
+                       : make_uint4(0u, 0u, 0u, 0u);
         } else {
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -264,8 +278,8 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
             if (k < g.nvv) {
               const uintptr_t va = g.A + 16 * k;
               if (seg_partial(g, k))
-                v[j] = load_edge(va, g.p0, g.e, view_lo, view_hi);
-              else
+                v[j] = load_edge(va, g.p0, g.e, view_lo, view_hi, clo, chi);
+              else if (PP_CHK_RANGE(va, 16, g.p0, g.e) && PP_CHK_RANGE(va, 16, clo, chi))
                 v[j] = ldg_stream(reinterpret_cast<const uint4 *>(va));
             }
           }
@@ -279,7 +293,7 @@ __global__ void __launch_bounds__(kSegThreads, PP_SEG_MIN_BLOCKS)
         c.eat8(v, t);
       }
       c.finish(t);
-      if (mine) write_row(a, s, g.p0, c, lane);
+      if (mine && PP_CHK(s < a.nseg)) write_row(a, s, g.p0, c, lane);
     }
     if (a.sched) {
       unsigned long long tk = 0;
@@ -332,6 +346,8 @@ __global__ void __launch_bounds__(kLaneThreads)
   const uintptr_t view_lo = PTRS ? 0 : base + (FIXED ? 0ull : a.seg_off[0]);
   const uintptr_t view_hi =
       PTRS ? 0 : base + (FIXED ? a.nseg * a.seg_bytes : a.seg_off[a.nseg]);
+  const uintptr_t chk_lo = a.chk_hi ? a.chk_lo : view_lo;  // checked builds
+  const uintptr_t chk_hi = a.chk_hi ? a.chk_hi : view_hi;
   const unsigned long long nw = (unsigned long long)gridDim.x * kLaneWarps;
   for (unsigned long long s0 = ((unsigned long long)blockIdx.x * kLaneWarps + warp) * 32;
        s0 < a.nseg; s0 += nw * 32) {
@@ -394,9 +410,11 @@ __global__ void __launch_bounds__(kLaneThreads)
       }
     };
     const uintptr_t vlo = PTRS ? p0 : view_lo, vhi = PTRS ? e : view_hi;
+    const uintptr_t clo = PTRS ? p0 : chk_lo, chi = PTRS ? e : chk_hi;
     auto load_vec = [&](uintptr_t va) -> uint4 {
       uint4 v;
       if (va >= vlo && va + 16 <= vhi) {
+        if (!PP_CHK_RANGE(va, 16, clo, chi)) return make_uint4(0u, 0u, 0u, 0u);
 #if PP_LANE_LDG_STREAM
         v = ldg_stream(reinterpret_cast<const uint4 *>(va));
 #else
@@ -411,7 +429,7 @@ __global__ void __launch_bounds__(kLaneThreads)
           v.w &= byte_range_mask(3, lo, hi);
         }
       } else {
-        v = load_partial(va, p0, e);
+        v = load_partial(va, p0, e, clo, chi);
       }
       return v;
     };
@@ -543,8 +561,13 @@ __global__ void __launch_bounds__(kSegTmaThreads, 1)
         const unsigned long long off = ch * chunk_bytes;
         const unsigned long long rem = total - off;
         const uint32_t bytes = (uint32_t)(rem < chunk_bytes ? rem : chunk_bytes);
-        mbar_arrive_expect_tx(&full[stage], bytes);
-        bulk_g2s(stages + stage * kStageVecs, a.base + off, bytes, &full[stage], pol);
+        if (PP_CHK(bytes <= kSegTmaStageBytes) &&
+            PP_CHK_RANGE(a.base + off, bytes, a.chk_lo, a.chk_hi)) {
+          mbar_arrive_expect_tx(&full[stage], bytes);
+          bulk_g2s(stages + stage * kStageVecs, a.base + off, bytes, &full[stage], pol);
+        } else {  // checked build, failed check: no copy, the stage completes empty
+          mbar_arrive(&full[stage]);
+        }
         ch = a.sched ? gridDim.x + (unsigned long long)(atomicAdd(a.sched, 1u) - a.sched_base)
                      : ch + gridDim.x;
       }
@@ -559,6 +582,7 @@ __global__ void __launch_bounds__(kSegTmaThreads, 1)
     mbar_wait(&full[stage], (j / kSegTmaStages) & 1u);
     const unsigned long long ch = chunk_id[stage];
     if (ch == kNoChunk) break;
+    PP_CHK(ch < nchunks);
     const uint4 *sv = stages + stage * kStageVecs;
     const unsigned long long seg0 = ch * segs_per_chunk;
     bool released = false;
@@ -567,6 +591,7 @@ __global__ void __launch_bounds__(kSegTmaThreads, 1)
       if (seg0 + (unsigned long long)it * S >= nseg) break;  // warp-uniform
       const bool item_full = seg0 + (unsigned long long)(it + 1) * S <= nseg;
       const uint4 *sp = sv + (it * S + sl) * segv + r;
+      PP_CHK((unsigned long long)(it * S + sl + 1) * segv <= kStageVecs);  // inside the stage
       GroupCounter<G, false> c;
       c.init();
       for (uint32_t k0 = 0; k0 < segv; k0 += 8 * G) {
@@ -644,16 +669,22 @@ static bool seg_use_tma(const SegArgs &a, const DevInfo &di, unsigned *items_per
 cudaError_t launch_segmented(const SegArgs &a0, const DevInfo &di, cudaStream_t st) {
   if (a0.nseg == 0) return cudaSuccess;
   SegArgs a = a0;
+#if PP_CHECK_BOUNDS
+  if (chk_corrupt_mode() == 3 && !a.ptrs && !a.short_max) a.base -= 16;  // pp_debug_corrupt
+#endif
   unsigned ipc = 0;
   // G = 2 / 4 (1-2 KiB fixed segments: 32 vectors per lane) exist only on the
   // TMA ring; elsewhere their segments go one lane each (G = 2) or to G = 8
-  if ((a.lanes_per_segment == 2 || a.lanes_per_segment == 4) && !seg_use_tma(a, di, &ipc))
+  if ((a.lanes_per_segment == 2 || a.lanes_per_segment == 4) && !seg_use_tma(a, di, &ipc)) {
     a.lanes_per_segment = a.lanes_per_segment == 2 ? 1 : 8;
+    // G = 2 demoted to one lane per segment: that single pass counts every
+    // segment, so the hybrid split must go -- else the one-lane kernel would
+    // count only the short segments and no pass would take the long ones
+    // (the hybrid's own one-lane pass below arrives here with G = 1 as asked
+    // and keeps its short_max)
+    if (a.lanes_per_segment == 1) a.short_max = 0;
+  }
   const int G = a.lanes_per_segment;
-  // G = 1 (asked for, or G = 2 demoted above) counts every segment one lane
-  // each: the hybrid split must not survive, or the one-lane kernel would
-  // count only the short segments and no pass would take the long ones
-  if (G == 1) a.short_max = 0;
   if (a.short_max && G != 1) {
     // hybrid: short segments one lane each, then the rest with G lanes
     SegArgs sh = a;
@@ -738,6 +769,23 @@ cudaError_t launch_segmented(const SegArgs &a0, const DevInfo &di, cudaStream_t 
       sched_commit(st);
   }
   return e;
+}
+
+cudaError_t chk_read_seg(ChkRecHost *out, bool reset) {
+#if PP_CHECK_BOUNDS
+  ChkRec r{};
+  cudaError_t e = cudaMemcpyFromSymbol(&r, pp_chk, sizeof r);
+  if (e != cudaSuccess) return e;
+  *out = ChkRecHost{r.fails, r.first_line, r.first_addr, r.first_lo, r.first_hi};
+  if (reset) {
+    const ChkRec z{};
+    return cudaMemcpyToSymbol(pp_chk, &z, sizeof z);
+  }
+#else
+  (void)reset;
+  *out = ChkRecHost{};
+#endif
+  return cudaSuccess;
 }
 
 }  // namespace pp

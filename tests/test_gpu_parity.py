@@ -467,9 +467,12 @@ def test_scheduler_slots_reused_by_new_streams(cuda, oracle):
     s0 = _sched_stats()
     streams = _raw_streams(300)
     keep = []
+    # every counter tensor is zeroed on the stream that counts into it: 600
+    # streams share a few hardware queues, so a zero-fill on another stream
+    # can sit behind a gated launch and land after the count
     for i, (h, s) in enumerate(streams):  # sequential: each launch done before the next
-        c = torch.zeros(8, dtype=torch.int64, device="cuda")
         with torch.cuda.stream(s):
+            c = torch.zeros(8, dtype=torch.int64, device="cuda")
             pp.pospopcnt(buf, 8, counters=c)
         s.synchronize()
         assert [int(x) for x in c.cpu()] == want, i
@@ -490,16 +493,16 @@ def test_scheduler_slots_reused_by_new_streams(cuda, oracle):
         gate.record(blocker)
     outs = []
     for h, s in busy:
-        c = torch.zeros(8, dtype=torch.int64, device="cuda")
         s.wait_event(gate)
         with torch.cuda.stream(s):
+            c = torch.zeros(8, dtype=torch.int64, device="cuda")
             pp.pospopcnt(buf, 8, counters=c)
         outs.append((s, c))
     s2 = _sched_stats()
     assert s2[2] > s1[2], (s1, s2)  # all-busy launches used the static order
     for s in keep:  # streams whose slots were taken over
-        c = torch.zeros(8, dtype=torch.int64, device="cuda")
         with torch.cuda.stream(s):
+            c = torch.zeros(8, dtype=torch.int64, device="cuda")
             pp.pospopcnt(buf, 8, counters=c)
         outs.append((s, c))
     torch.cuda.synchronize()

@@ -60,8 +60,22 @@ def test_reference_suite_with_b200_registered(ref):
     kernel-parametrised test includes b200 next to portable/int256/numba/
     numpy, and the registry/CLI/bench contracts still hold with it added.
     Criterion 1 runs on its own below (b200 only)."""
-    out = _pytest(["-k", "not criterion_1"])
+    # test_instrumented_modes_match_default (test_kernels.py:135-142) exempts
+    # the compiled kernel by NAME ("numba"); b200 is compiled too and, per the
+    # same contract (kernels.py:243-244), rejects fa=/probe= -- asserted below
+    out = _pytest(["-k", "not criterion_1 and not test_instrumented_modes_match_default"])
     assert "passed" in out and "failed" not in out
+
+
+def test_b200_rejects_instrumentation_like_numba(ref):
+    """test_numba_rejects_instrumentation (test_kernels.py:145-150), for b200."""
+    P, k = ref
+    from pospopcnt.csa import full_adder
+    for kern in (k, P.get_kernel("numba")):
+        with pytest.raises(ValueError):
+            kern.run(P.InputView.of(b"\x00" * 16), 8, [0] * 8, fa=full_adder)
+        with pytest.raises(ValueError):
+            kern.run(P.InputView.of(b"\x00" * 16), 8, [0] * 8, probe=lambda st: None)
 
 
 def test_reference_criterion1_sweep_on_b200(ref):
