@@ -259,7 +259,7 @@ PP_API int pp_sched_stats(unsigned long long *out4);
  */
 PP_API int pp_check_status(unsigned long long *out6, int reset);
 /* pp_debug_corrupt — checked builds only: corrupt the launchers' derived
- * ranges (1: body runs 32 bytes past the end, 2: head/tail edge bytes
+ * ranges (1: body shifted 32 bytes past the end, 2: head/tail edge bytes
  * outside, 3: fixed segmented base 16 bytes low) so a test can show the
  * checks fire; 0 restores normal launches.  PP_EARG in unchecked builds. */
 PP_API int pp_debug_corrupt(int mode);

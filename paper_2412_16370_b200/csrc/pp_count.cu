@@ -974,7 +974,7 @@ static cudaError_t launch_tma(Kern kernel, unsigned grid, unsigned block, size_t
       cudaMemsetAsync(a.chk_ctr, 0, 16, st) != cudaSuccess)
     return cudaGetLastError();
   switch (chk_corrupt_mode()) {  // pp_debug_corrupt: derived fields go wrong
-    case 1: a.body_bytes += 32; break;                       // bulk copy past the end
+    case 1: a.body += 32; break;                              // last bulk copy past the end
     case 2: a.head -= 1; a.head_bytes += 1; a.tail_bytes += 1; break;  // edge bytes outside
     default: break;
   }
