@@ -942,11 +942,11 @@ def main_gpu(args):
 
     # C5 strong scaling beside the weak-scaling headline: the fixed 64 GiB
     # array split over the N ranks, exact against the reference's own total
-    strong = None
+    strong_c5 = None
     if args.strong_c5 and cfg == "c2":
         del buf
         torch.cuda.empty_cache()
-        strong = run_strong_c5(args, lib, world, rank, dev, st, use_dist, peers)
+        strong_c5 = run_strong_c5(args, lib, world, rank, dev, st, use_dist, peers)
 
     if rank == 0:
         line = {
@@ -978,7 +978,7 @@ def main_gpu(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_fanout": e2e_fanout,
-            "strong_c5": strong,
+            "strong_c5": strong_c5,
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
             "exact": exact,

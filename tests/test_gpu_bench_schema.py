@@ -30,6 +30,8 @@ def test_bench_line_contract(cuda):
     assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3
     assert d["unit"] == "GB/s" and d["higher_is_better"] is True and d["dtype"] == "u8"
     assert d["value"] > 1000 and d["exact"] is True
+    # C2 is per-GPU work (weak scaling), whatever objects ride along (strong_c5)
+    assert d["scaling"] == "weak"
     assert abs(d["value"] - d["config"]["bytes_per_step_all_gpus"] / d["ms_per_step"] / 1e6) \
         < 0.01 * d["value"]
     r = d["roofline"]
@@ -59,6 +61,7 @@ def test_reference_arm_contract():
              "--no-strong-c5")
     # same workload description as the GPU arm: the driver matches the lines
     assert d["config"] == g["config"] and d["metric"] == g["metric"]
+    assert d["scaling"] == g["scaling"] == "weak"
     assert d["impl"] == "reference" and d["unit"] == "GB/s" and d["value"] > 0
     assert d["cpu_baseline"]["value"] == d["value"] and d["e2e"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["gpu_launches"] == 0
