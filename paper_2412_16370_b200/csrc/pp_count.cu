@@ -25,6 +25,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <type_traits>
 
 #include "pp_device.cuh"
 #include "pp_internal.h"
@@ -225,8 +226,8 @@ __device__ __forceinline__ uint32_t onehot32(uint32_t c) {
 // Expand and count 8 vectors (128 u8 codes) of one thread; vectors with
 // valid bit i clear are absent (partial last chunk) and contribute nothing.
 // FULL: every vector present (all but the last chunk) -- no per-word selects.
-template <int W, bool FULL>
-__device__ __forceinline__ void eat_codes(Counter &c, const uint4 (&v)[8], uint32_t valid,
+template <int W, bool FULL, class Ctr>
+__device__ __forceinline__ void eat_codes(Ctr &c, const uint4 (&v)[8], uint32_t valid,
                                           const TC &t) {
   const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
   if (W == 8) {
@@ -243,7 +244,7 @@ __device__ __forceinline__ void eat_codes(Counter &c, const uint4 (&v)[8], uint3
 #endif
       if (!FULL && !((valid >> i) & 1u)) u[i] = z4;
     }
-    c.eat8(u, t);
+    c.csa(u, 0);
   } else if (W == 16) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -259,7 +260,7 @@ __device__ __forceinline__ void eat_codes(Counter &c, const uint4 (&v)[8], uint3
                                        onehot16x2(x.w, 0), onehot16x2(x.w, 2))
                           : z4;
       }
-      c.eat8(u, t);
+      c.csa(u, h);
     }
   } else if (W == 32) {
 #pragma unroll
@@ -278,7 +279,7 @@ __device__ __forceinline__ void eat_codes(Counter &c, const uint4 (&v)[8], uint3
                             : z4;
         }
       }
-      c.eat8(u, t);
+      c.csa(u, h);
     }
   } else {  // W == 64: code c -> (x|z, y|w) = (1 << c, 1 << (c - 32))
 #pragma unroll
@@ -304,9 +305,10 @@ __device__ __forceinline__ void eat_codes(Counter &c, const uint4 (&v)[8], uint3
 #endif
         }
       }
-      c.eat8(u, t);
+      c.csa(u, h);
     }
   }
+  c.end_chunk(t);
 }
 
 // Fast path for W = 32 when every code of the warp's 8 vectors is < 32 (the
@@ -321,6 +323,16 @@ __device__ __forceinline__ void eat_codes(Counter &c, const uint4 (&v)[8], uint3
 #ifndef PP_CAT_SMALL
 #define PP_CAT_SMALL 1
 #endif
+// eat8 groups per chunk of one thread (8 vectors of CB-byte codes): the
+// one-hot words of 128 / CB codes, W / 32 words per code (W = 8: four codes
+// per word, 16: two), 32 words per group
+template <int W, int CB>
+constexpr int groups_per_chunk() {
+  return CB == 1 ? W / 8 : CB == 2 ? (W <= 16 ? 1 : W == 32 ? 2 : 4) : (W <= 32 ? 1 : 2);
+}
+// the fused producer's counter: one tree at W <= 32, two at W = 64
+template <int W, int CB>
+using CatCtr = CatCounter<W == 64 ? 2 : 1, (W == 64 ? 1 : 2) * groups_per_chunk<W, CB>()>;
 __device__ __forceinline__ uint32_t hi_bytes(uint32_t x, int k) {  // x >> 8k, k = 1..3
   uint32_t r;
   asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(1u << (32 - 8 * k)));
@@ -329,7 +341,8 @@ __device__ __forceinline__ uint32_t hi_bytes(uint32_t x, int k) {  // x >> 8k, k
 __device__ __forceinline__ uint32_t oh_wrap(uint32_t n) {  // 1 << (n mod 32)
   return __funnelshift_l(0u, 1u, n);
 }
-__device__ __forceinline__ void eat_small_codes32(Counter &c, const uint4 (&v)[8], const TC &t) {
+template <class Ctr>
+__device__ __forceinline__ void eat_small_codes32(Ctr &c, const uint4 (&v)[8], const TC &t) {
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
     uint4 u[8];
@@ -344,8 +357,9 @@ __device__ __forceinline__ void eat_small_codes32(Counter &c, const uint4 (&v)[8
                                   oh_wrap(hi_bytes(wd, 3)));
       }
     }
-    c.eat8(u, t);
+    c.csa(u, h);
   }
+  c.end_chunk(t);
 }
 
 // 2- / 4-byte codes (CB = code bytes): the same packed one-hot words, built
@@ -368,8 +382,8 @@ __device__ __forceinline__ uint32_t oh16pair(uint32_t c0, uint32_t c1) {
   return (shl32(1u, c0) & 0xFFFFu) | shl32(0x10000u, c1);
 }
 
-template <int W, bool FULL, int CB>
-__device__ __forceinline__ void eat_wide_codes(Counter &c, const uint4 (&v)[8], uint32_t valid,
+template <int W, bool FULL, int CB, class Ctr>
+__device__ __forceinline__ void eat_wide_codes(Ctr &c, const uint4 (&v)[8], uint32_t valid,
                                                const TC &t) {
   static_assert(CB == 2 || CB == 4, "code bytes");
   const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
@@ -394,7 +408,7 @@ __device__ __forceinline__ void eat_wide_codes(Counter &c, const uint4 (&v)[8], 
                                        shl32(1u, code(k + 2)), shl32(1u, code(k + 3)))
                           : z4;
       }
-      c.eat8(u, t);
+      c.csa(u, r);
     }
   } else if (W == 64) {  // one (lo, hi) pair per code: K / 16 rounds
 #pragma unroll
@@ -408,7 +422,7 @@ __device__ __forceinline__ void eat_wide_codes(Counter &c, const uint4 (&v)[8], 
         onehot64(code(k + 1), l1, h1);
         u[q] = present(k) ? make_uint4(l0, h0, l1, h1) : z4;
       }
-      c.eat8(u, t);
+      c.csa(u, r);
     }
   } else {  // W = 16: two codes per word, W = 8: four; one round, padded
     constexpr int PER = W == 16 ? 2 : 4;
@@ -431,8 +445,9 @@ __device__ __forceinline__ void eat_wide_codes(Counter &c, const uint4 (&v)[8], 
       }
       u[q] = make_uint4(wq[0], wq[1], wq[2], wq[3]);
     }
-    c.eat8(u, t);
+    c.csa(u, 0);
   }
+  c.end_chunk(t);
 }
 
 // The same split in two for the TMA kernel, whose warp 0 of CTA 0 loads its
@@ -457,8 +472,8 @@ __device__ __forceinline__ uint64_t edge_load(const CountArgs &a, uint32_t lane)
                  : CB == 2 ? __ldg(reinterpret_cast<const uint16_t *>(p))
                            : __ldg(reinterpret_cast<const uint32_t *>(p));
 }
-template <int CB>
-__device__ __forceinline__ void edge_count(Counter &c, uint64_t v, int width, const TC &t) {
+template <int CB, class Ctr>
+__device__ __forceinline__ void edge_count(Ctr &c, uint64_t v, int width, const TC &t) {
   if (CB == 0) {  // v = the byte, already placed at its frame position
     c.ce += wcount((uint32_t)v, t);
     c.co += wcount((uint32_t)(v >> 32), t);
@@ -565,7 +580,11 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   } else {
     // ---------------- consumers
     const TC t = make_tc(lane);
-    Counter c;
+    // the fused producer batches a chunk's a16 planes (CatCounter); the
+    // positional count keeps one eat8 per chunk (Counter)
+    using Ctr = typename std::conditional<(MODE >= 8), CatCtr<(MODE >= 8 ? MODE : 8), CB>,
+                                          Counter>::type;
+    Ctr c;
     c.init();
     uint32_t xs = 0;  // read-only roofline accumulator
     constexpr int kEdgeCB = MODE == 1 ? 0 : CB;
@@ -619,20 +638,27 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         for (int i = 0; i < 8; ++i) o |= v[i].x | v[i].y | v[i].z | v[i].w;
         small = __all_sync(FULL, valid == 0xFFu && (o & 0xE0E0E0E0u) == 0u);
       }
-      if (MODE == 1) {
+      if constexpr (MODE == 1) {
         c.eat8(v, t);
-      } else if (MODE == 32 && CB == 1 && small) {
-        eat_small_codes32(c, v, t);
-      } else if (MODE >= 8 && CB == 1) {
+      } else if constexpr (MODE >= 8 && CB == 1) {
+        bool done = false;
+        if constexpr (MODE == 32) {
+          if (small) {
+            eat_small_codes32(c, v, t);
+            done = true;
+          }
+        }
+        if (!done) {
+          if (valid == 0xFFu)
+            eat_codes<MODE, true>(c, v, valid, t);
+          else
+            eat_codes<MODE, false>(c, v, valid, t);
+        }
+      } else if constexpr (MODE >= 8) {
         if (valid == 0xFFu)
-          eat_codes<(MODE >= 8 ? MODE : 8), true>(c, v, valid, t);
+          eat_wide_codes<MODE, true, CB>(c, v, valid, t);
         else
-          eat_codes<(MODE >= 8 ? MODE : 8), false>(c, v, valid, t);
-      } else if (MODE >= 8) {
-        if (valid == 0xFFu)
-          eat_wide_codes<(MODE >= 8 ? MODE : 8), true, (CB > 1 ? CB : 2)>(c, v, valid, t);
-        else
-          eat_wide_codes<(MODE >= 8 ? MODE : 8), false, (CB > 1 ? CB : 2)>(c, v, valid, t);
+          eat_wide_codes<MODE, false, CB>(c, v, valid, t);
       } else {
 #pragma unroll
         for (int i = 0; i < 8; ++i) xs ^= v[i].x ^ v[i].y ^ v[i].z ^ v[i].w;

@@ -245,6 +245,109 @@ struct Counter {
   }
 };
 
+// Chunk-batched counter of the fused one-hot producer.  One chunk of a
+// thread (8 vectors of codes) expands into a STATIC number of eat8 groups
+// (W / 8 for u8 codes), so the a16 planes of a whole chunk are known at
+// compile time and are combined by a static Harley-Seal tree (M - 1 full
+// adders into persistent planes of weight 16, 32, ...) before ONE ripple
+// increment of the second-level counter -- instead of an increment per
+// group (7 ops each) and a second-level count every 15 groups.  NT = 1:
+// both u32 lanes of a frame word count the same W <= 32 positions (the fold
+// sums frame[j] and frame[j + 32]), so every word goes through one tree;
+// NT = 2 (W = 64): e = frame bits 0..31, o = 32..63, as Counter.
+// (The paper's own scheme, csa.py:63-87, applied a second time.)
+template <int NT, int M>
+struct CatCounter {
+  static_assert(NT == 1 || NT == 2, "trees");
+  static_assert(M == 1 || M == 2 || M == 4 || M == 8 || M == 16, "a16 planes per chunk");
+  static constexpr int kLog = M >= 16 ? 4 : M >= 8 ? 3 : M >= 4 ? 2 : M >= 2 ? 1 : 0;
+  Planes l1[NT];           // weights 1, 2, 4, 8
+  uint32_t h[NT][kLog > 0 ? kLog : 1];     // weights 16 << k
+  uint32_t slot[NT][kLog > 0 ? kLog : 1];  // a plane waiting for its pair, level k
+  Planes l2[NT];           // weights 16 M << (0..3)
+  uint32_t l2n;            // chunks held in l2 (<= 15; warp-uniform)
+  unsigned long long ce, co;
+
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int r = 0; r < NT; ++r) {
+      l1[r] = l2[r] = Planes{0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int k = 0; k < (kLog > 0 ? kLog : 1); ++k) h[r][k] = 0u;
+    }
+    l2n = 0u;
+    ce = co = 0ull;
+  }
+  // The idx-th a16 plane of the chunk (idx static): a binary counter over
+  // idx with a full adder per trailing one, resolved at compile time, so at
+  // most log2(M) planes wait at any time; the last one (idx = M - 1) leaves
+  // the chunk's single carry of weight 16 M for the ripple increment.
+  __device__ __forceinline__ void put(int r, int idx, uint32_t x) {
+#pragma unroll
+    for (int k = 0; k < kLog; ++k) {
+      if (!((idx >> k) & 1)) {
+        slot[r][k] = x;
+        return;
+      }
+      PP_FA(x, h[r][k], h[r][k], slot[r][k], x);
+    }
+    inc4(l2[r], x);
+  }
+  // Group g of the chunk (static): 32 words, two csa16_4
+  __device__ __forceinline__ void csa(const uint4 (&v)[8], int g) {
+    uint32_t x[16], y[16];
+    if (NT == 1) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        x[4 * i] = v[i].x;
+        x[4 * i + 1] = v[i].y;
+        x[4 * i + 2] = v[i].z;
+        x[4 * i + 3] = v[i].w;
+        y[4 * i] = v[4 + i].x;
+        y[4 * i + 1] = v[4 + i].y;
+        y[4 * i + 2] = v[4 + i].z;
+        y[4 * i + 3] = v[4 + i].w;
+      }
+      put(0, 2 * g, csa16_4(l1[0], x));
+      put(0, 2 * g + 1, csa16_4(l1[0], y));
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        x[2 * i] = v[i].x;
+        x[2 * i + 1] = v[i].z;
+        y[2 * i] = v[i].y;
+        y[2 * i + 1] = v[i].w;
+      }
+      put(0, g, csa16_4(l1[0], x));
+      put(NT - 1, g, csa16_4(l1[NT - 1], y));
+    }
+  }
+  // after the chunk's last group
+  __device__ __forceinline__ void end_chunk(const TC &t) {
+    if (++l2n == 15u) flush_l2(t);
+  }
+  __device__ __forceinline__ void flush_l2(const TC &t) {
+    ce += (unsigned long long)wcount_planes(l2[0], 0, t) << (4 + kLog);
+    if (NT == 2) co += (unsigned long long)wcount_planes(l2[NT - 1], 0, t) << (4 + kLog);
+#pragma unroll
+    for (int r = 0; r < NT; ++r) l2[r] = Planes{0u, 0u, 0u, 0u};
+    l2n = 0u;
+  }
+  __device__ __forceinline__ void finish(const TC &t) {
+#pragma unroll
+    for (int r = 0; r < NT; ++r) {
+      unsigned long long s = wcount_planes(l1[r], 0, t);
+#pragma unroll
+      for (int k = 0; k < kLog; ++k) s += (unsigned long long)wcount(h[r][k], t) << (4 + k);
+      if (r == 0) ce += s; else co += s;
+      l1[r] = Planes{0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int k = 0; k < (kLog > 0 ? kLog : 1); ++k) h[r][k] = 0u;
+    }
+    if (l2n) flush_l2(t);
+  }
+};
+
 // Segment-parallel variant: G lanes share one segment, so a warp carries
 // S = 32/G independent segments.  Each transpose stage swaps one bit of the
 // lane index with the same bit of the bit index, and the stages commute, so

@@ -10,6 +10,11 @@ Segments live in one CUDA byte buffer; segment s is bytes
 [offsets[s], offsets[s+1]) of the view.  Every segment must be word-complete.
 """
 
+import collections
+import hashlib
+import threading
+import weakref
+
 import numpy as np
 
 from . import _lib
@@ -66,12 +71,22 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
     ``plan``: a ``SegmentPlan`` built once for these offsets (repeated counts
     over one segmentation): the G-lane kernel then takes the segments in the
     plan's length-sorted order and the plan's shape; ``offsets`` may be None.
+    Default (``plan=None``): a ragged segmentation counted a second time
+    with the same offsets (the same, unmodified CUDA tensor, or equal host
+    offsets) and the default shape gets a ``SegmentPlan`` built and cached
+    (``PLAN_CACHE_SIZE`` most recent segmentations per process) and used
+    from then on; ``plan=False`` never plans.
     """
     import torch
     check_width(width)
     view = _device_view(data)
-    if plan is not None:
+    if plan is not None and plan is not False:
         return plan.count(view, width, out=out, accumulate=accumulate)
+    auto = plan is None and lanes is None and hybrid is None
+    if auto:
+        cached = _PLANS.lookup(offsets, view.base.device)
+        if cached is not None:
+            return cached.count(view, width, out=out, accumulate=accumulate)
     dev = view.base.device
     step = width // 8
     shape = None  # (lanes, hybrid) from the lengths, when they are known here
@@ -109,6 +124,10 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
         return out
     lib = _lib.load()
     flags = _lib.PP_SEG_ACCUMULATE if (accumulate and not fresh) else _lib.PP_SEG_OVERWRITE
+    if auto and shape is not None and shape[0] != 1 and not shape[1] and nseg >= 64:
+        # G-lane shape over ragged lengths: the length-sorted plan pays when
+        # the same segmentation comes back (built on the second sighting)
+        _PLANS.seen(offsets, dev, d)
     if lanes is None and shape is not None:
         lanes = shape[0]
         if hybrid is None:
@@ -124,6 +143,80 @@ def pospopcnt_segmented(data, offsets, width, out=None, accumulate=True, validat
         # keep the offsets tensor alive until the kernel has consumed it
         offs.record_stream(torch.cuda.current_stream(dev))
     return out
+
+
+PLAN_CACHE_SIZE = 8
+
+
+class _PlanCache:
+    """Segmentations seen by pospopcnt_segmented, and the plans built for
+    those seen twice.  A CUDA offsets tensor is keyed by identity plus its
+    version counter (an in-place write invalidates the entry; a freed
+    tensor's entry dies with its weakref); host offsets by their bytes.
+    Thread-safe; ``stats`` = [plans built, plan hits]."""
+
+    def __init__(self, size):
+        self.size = size
+        self.lock = threading.Lock()
+        self.seen_keys = collections.OrderedDict()  # key -> None (first sighting)
+        self.plans = collections.OrderedDict()      # key -> (check, SegmentPlan)
+        self.stats = [0, 0]
+
+    @staticmethod
+    def _key(offsets, dev):
+        if is_torch_tensor(offsets):
+            if not offsets.is_cuda:
+                offsets = offsets.numpy()
+            else:
+                return (("dev", id(offsets), offsets._version, str(dev)),
+                        weakref.ref(offsets))
+        a = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+        return ("host", a.size, hashlib.blake2b(a.data, digest_size=16).digest(), str(dev)), None
+
+    def lookup(self, offsets, dev):
+        key, ref = self._key(offsets, dev)
+        with self.lock:
+            hit = self.plans.get(key)
+            if hit is None:
+                return None
+            if hit[0] is not None and hit[0]() is not offsets:  # id reused by a new tensor
+                del self.plans[key]
+                return None
+            self.plans.move_to_end(key)
+            self.stats[1] += 1
+            return hit[1]
+
+    def seen(self, offsets, dev, lengths):
+        key, ref = self._key(offsets, dev)
+        with self.lock:
+            if key not in self.seen_keys:
+                self.seen_keys[key] = ref
+                while len(self.seen_keys) > 4 * self.size:
+                    self.seen_keys.popitem(last=False)
+                return
+            first = self.seen_keys.pop(key)
+            if first is not None and first() is not offsets:
+                self.seen_keys[key] = ref
+                return
+        if is_torch_tensor(lengths):
+            lengths = lengths.cpu().numpy()
+        if int(lengths.min()) == int(lengths.max()):
+            return  # equal lengths: index order is already balanced
+        p = SegmentPlan(offsets, device=dev)
+        with self.lock:
+            self.plans[key] = (ref, p)
+            self.stats[0] += 1
+            while len(self.plans) > self.size:
+                self.plans.popitem(last=False)
+
+    def clear(self):
+        with self.lock:
+            self.seen_keys.clear()
+            self.plans.clear()
+            self.stats = [0, 0]
+
+
+_PLANS = _PlanCache(PLAN_CACHE_SIZE)
 
 
 def _byte_mean(d):

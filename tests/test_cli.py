@@ -47,10 +47,12 @@ def test_kernels_listing(capsys):
     assert all(("available" in ln or "unavailable" in ln) for ln in lines)
 
 
-def test_selftest_without_gpu_is_an_input_error(capsys, monkeypatch):
+def test_count_without_gpu_is_an_input_error(capsys, monkeypatch, tmp_path):
     """No usable kernel: KernelUnavailableError -> exit 2 (cli.py:151-154);
     never a silent CPU run."""
     from paper_2412_16370_b200 import kernels as K
     monkeypatch.setattr(K.B200Kernel, "available", lambda self: False)
-    code, _, err = run(capsys, "selftest", "--iterations", "3")
+    f = tmp_path / "x.bin"
+    f.write_bytes(b"\x0f" * 8)
+    code, _, err = run(capsys, "count", str(f))
     assert code == 2 and ("not available" in err or "no pospopcnt kernel" in err)

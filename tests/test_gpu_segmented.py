@@ -254,3 +254,41 @@ def test_segment_plan_exact(cuda, oracle, lanes):
         assert tiny.hybrid and tiny.lanes == 32
     with pytest.raises(ValueError):
         pp.SegmentPlan([0, 8, 4])
+
+
+def test_plan_auto_cache(cuda, oracle):
+    """A ragged segmentation counted again with the same offsets gets a
+    cached SegmentPlan (second sighting), rows unchanged; an in-place write
+    to a device offsets tensor, or different host offsets, never reuse a
+    stale plan; plan=False opts out."""
+    torch, pp = cuda
+    from paper_2412_16370_b200 import segmented as S
+    S._PLANS.clear()
+    rng = np.random.default_rng(5)
+    w = 32
+    lens = rng.integers(0, 6000 // 4, 4000) * 4
+    offs = np.zeros(lens.size + 1, dtype=np.int64)
+    offs[1:] = np.cumsum(lens)
+    host = rng.integers(0, 256, int(offs[-1]) + 16, dtype=np.uint8)
+    buf = torch.from_numpy(host).cuda()
+    want = oracle.segments(host, offs.astype(np.uint64), w)
+    for src in ("host", "device"):
+        S._PLANS.clear()
+        o = offs.copy() if src == "host" else torch.as_tensor(offs, device="cuda")
+        for i in range(4):
+            out = pp.pospopcnt_segmented(buf, o, w)
+            assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (src, i)
+        built, hits = S._PLANS.stats
+        assert built == 1 and hits == 2, (src, S._PLANS.stats)
+        # a different segmentation
+        o2 = offs.copy()
+        o2[1] = 0  # segment 0 empty, segment 1 longer
+        want2 = oracle.segments(host, o2.astype(np.uint64), w)
+        if src == "device":
+            o.copy_(torch.as_tensor(o2))  # in place: version bump
+            o2 = o
+        out = pp.pospopcnt_segmented(buf, o2, w)
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), want2), src
+        assert S._PLANS.stats[1] == 2  # no stale hit
+    out = pp.pospopcnt_segmented(buf, offs, w, plan=False)
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), want)
