@@ -100,6 +100,18 @@ def load_traffic(kernel_key, input_bytes):
         return None, None
 
 
+def load_alu(kernel_key):
+    """ALU-pipe lane-instructions per input byte (= per u8 code) of a fused
+    producer kernel, from the committed ncu capture (profiles/ncu_alu.json)."""
+    p = os.path.join(ROOT, "profiles", "ncu_alu.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)[kernel_key]
+        return round(d["alu_warp_inst"] * 32 / d["input_bytes"], 4)
+    except Exception:  # noqa: BLE001
+        return None
+
+
 class ClockSampler:
     """SM clocks and throttle reasons sampled (NVML, ~1 ms period) while the
     timed region runs; mark() brackets the region on the host clock.  Falls
@@ -834,7 +846,7 @@ def main_gpu(args):
     achieved = per_step_bytes / (k_ms / 1e3) / 1e9
     seg_tma = os.environ.get("PP_SEG_PATH", "") != "ldg" and view_ptr % 16 == 0
     kernel_key = (("pp_segtma_kernel<8>" if seg_tma else "pp_seg_kernel") if seg_out is not None else
-                  "pp_cat_kernel<1>" if categorical else "pp_tma_kernel<1>")
+                  f"pp_tma_kernel<{w}, 16>" if categorical else "pp_tma_kernel<1>")
     traffic, traffic_ratio = load_traffic(kernel_key, per_step_bytes)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -845,6 +857,24 @@ def main_gpu(args):
                 # B200 HBM3e datasheet figure (HGX; 8 TB/s DGX), stated as such
                 "spec_peak_gbs": SPEC_HBM_GBS,
                 "frac_of_spec": round(achieved / SPEC_HBM_GBS, 4)}
+    if categorical:
+        # the fused producer is ALU-bound, not HBM-bound (profiles/r2_cat_ncu.md):
+        # ALU-pipe lane-ops per code (ncu, this build) x codes/s (live) against
+        # 148 SMs x 64 lane-ops/clk x the SM clock sampled in the region
+        alu = load_alu(kernel_key)
+        if alu is not None:
+            mhz = clk.summary().get("sm_mhz") or 1965.0
+            ops = alu * per_step_bytes / (k_ms / 1e3) / 1e12
+            apeak = 148 * 64 * mhz * 1e6 / 1e12
+            hbm = dict(roofline)
+            roofline = {"bound": "alu", "achieved": round(ops, 3), "peak": round(apeak, 3),
+                        "unit": "T lane-ops/s", "frac": round(ops / apeak, 4),
+                        "traffic": traffic, "kernel": kernel_key,
+                        "alu_lane_ops_per_code_ncu": alu,
+                        "peak_source": f"148 SMs x 64 ALU-pipe lane-ops/clk x {mhz:.0f} MHz "
+                                       "(median SM clock in the timed region)",
+                        "hbm": {k: hbm[k] for k in ("achieved", "peak", "unit", "frac",
+                                                    "readonly_roofline_gbs")}}
     if seg_out is not None:
         seg_bytes_out = (nbytes // 4096) * w * 8
         roofline["algorithmic_bytes_per_launch"] = per_step_bytes + seg_bytes_out

@@ -333,10 +333,17 @@ constexpr int groups_per_chunk() {
 // the fused producer's counter: one tree at W <= 32, two at W = 64
 template <int W, int CB>
 using CatCtr = CatCounter<W == 64 ? 2 : 1, (W == 64 ? 1 : 2) * groups_per_chunk<W, CB>()>;
+#ifndef PP_CAT_SMALL_MULHI  // 0: plain shifts (ALU) for bytes 1-3 (A/B)
+#define PP_CAT_SMALL_MULHI 1
+#endif
 __device__ __forceinline__ uint32_t hi_bytes(uint32_t x, int k) {  // x >> 8k, k = 1..3
+#if PP_CAT_SMALL_MULHI
   uint32_t r;
   asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(1u << (32 - 8 * k)));
   return r;
+#else
+  return x >> (8 * k);
+#endif
 }
 __device__ __forceinline__ uint32_t oh_wrap(uint32_t n) {  // 1 << (n mod 32)
   return __funnelshift_l(0u, 1u, n);
