@@ -224,7 +224,9 @@ def host_threads():
 def config_dict(cfg, world, per_gpu_bytes, job_bytes, w):
     """The workload description both arms print (identical dicts, so the
     driver can match the reference arm's line to this arm's)."""
-    kind, _, _, desc = CONFIGS[cfg]
+    kind, w0, _, desc = CONFIGS[cfg]
+    if w != w0:  # --width override of C2's word width
+        desc = desc.replace(f"w={w0},", f"w={w},", 1)
     if cfg == "c4seg":
         par = f"dp{world} (segment ranges; rows stay on their rank, no exchange)"
     else:
