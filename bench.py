@@ -455,6 +455,10 @@ def run_strong_c5(args, lib, world, rank, dev, st, use_dist, peers):
     return {"value": round(gbs, 1), "unit": "GB/s", "ms_per_step": round(t_ms / steps, 4),
             "steps": steps, "warmup": warm, "n_gpus": world, "scaling": "strong",
             "bytes_total": total, "bytes_per_gpu": n,
+            "launch": ("pp_count_ex(..., PP_COUNT_INPUT_READY): inputs written once before "
+                       "the first count, so a step's loads may overlap the previous step's tail"
+                       if count_flags and not categorical and seg_out is None and not fused
+                       else "plain launches"),
             "exchange": ("fused in-kernel peer adds" if fused else
                          "NCCL allreduce per step" if use_dist else "none (one GPU)"),
             "hbm_frac_per_gpu": round(gbs / world / load_peaks()[0], 4),
@@ -570,6 +574,9 @@ def main_gpu(args):
     red_ev = [torch.cuda.Event() for _ in range(2)]
     side = torch.cuda.Stream(dev) if use_dist else None
     nstep = [0]
+    # the inputs are written once, before any count: each step's loads may
+    # overlap the previous step's tail (pp_count_ex, PP_COUNT_INPUT_READY)
+    count_flags = _lib.PP_COUNT_INPUT_READY if args.input_ready else 0
     seg_out = None
     if cfg == "c4seg":
         seg = 4096
@@ -593,7 +600,8 @@ def main_gpu(args):
                 _lib.check(lib.pp_count_categories(view_ptr, nbytes, 1, w,
                                                    counters2[b].data_ptr(), sp))
             else:
-                _lib.check(lib.pp_count(view_ptr, nbytes, w, counters2[b].data_ptr(), sp))
+                _lib.check(lib.pp_count_ex(view_ptr, nbytes, w, counters2[b].data_ptr(),
+                                           count_flags, sp))
         if use_dist and seg_out is None:  # segmented rows stay on their rank
             count_ev[b].record(st)
             side.wait_event(count_ev[b])
@@ -1111,6 +1119,8 @@ def main():
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-min-time", type=float, default=5.0)
+    ap.add_argument("--no-input-ready", dest="input_ready", action="store_false",
+                    help="count with plain pp_count (loads wait for the previous kernel)")
     ap.add_argument("--no-strong-c5", dest="strong_c5", action="store_false",
                     help="skip the C5 strong-scaling object of the c2 line")
     args = ap.parse_args()

@@ -92,6 +92,22 @@ PP_API int pp_count(const void *data, size_t nbytes, int width,
              unsigned long long *counters, void *stream);
 
 /*
+ * pp_count_ex — pp_count with flags.  PP_COUNT_INPUT_READY: the caller
+ * vouches that the input was complete before the previous kernel on
+ * `stream` started (that kernel does not write it).  Every count launch
+ * uses programmatic dependent launch; with this flag its bulk copies start
+ * while the previous kernel drains instead of after it completes (back-to-
+ * back counts of independent inputs: the next input's first loads overlap
+ * the previous launch's tail).  Counter updates still wait for the previous
+ * kernel.  Without the flag (pp_count) the loads wait, so a producer kernel
+ * of the input that itself uses programmatic launch is always safe.
+ * Replaces: as pp_count (kernels.py:242-270, 315-333).
+ */
+#define PP_COUNT_INPUT_READY 1u
+PP_API int pp_count_ex(const void *data, size_t nbytes, int width,
+                unsigned long long *counters, unsigned int flags, void *stream);
+
+/*
  * pp_count_sync — pp_count over DEVICE bytes with the result added into HOST
  * counters: one call = zero a per-thread device scratch, count, copy the w
  * counters back, synchronise `stream`.  The reference's list-returning call

@@ -24,6 +24,7 @@ PP_MAX_TARGETS = 16        # pp_count_multi: counter arrays per call
 PP_MAX_FANOUT = 16         # pp_count_host_multi: devices per call
 PP_IPC_HANDLE_BYTES = 72   # pp_ipc_handle: CUDA IPC handle + offset in the allocation
 ABI_VERSION = 1
+PP_COUNT_INPUT_READY = 1   # pp_count_ex: loads need not wait for the previous kernel
 
 # name -> (restype, argtypes); mirrors include/pospopcnt_b200.h
 _vp, _sz, _int, _u64, _u32 = (ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
@@ -34,6 +35,7 @@ SIGNATURES = {
     "pp_last_error": (ctypes.c_char_p, []),
     "pp_device_info": (_int, [_int, _vp, _vp, _vp]),
     "pp_count": (_int, [_vp, _sz, _int, _vp, _vp]),
+    "pp_count_ex": (_int, [_vp, _sz, _int, _vp, _u32, _vp]),
     "pp_count_host": (_int, [_vp, _sz, _int, _vp]),
     "pp_count_sync": (_int, [_vp, _sz, _int, _vp, _vp]),
     "pp_count_host_multi": (_int, [_vp, _sz, _int, _vp, _vp, _int]),

@@ -106,12 +106,14 @@ std::mutex g_ipc_m;
 std::map<void *, void *> g_ipc_base;
 
 int count_device(const void *data, size_t nbytes, int width, unsigned long long *counters,
-                 cudaStream_t st, const pp::DevInfo &di, bool raw_frame = false) {
+                 cudaStream_t st, const pp::DevInfo &di, bool raw_frame = false,
+                 unsigned int flags = 0) {
   pp::CountArgs a{};
   const pp::LoadPath path = load_path();
   pp::split_range(static_cast<const uint8_t *>(data), nbytes, pp::count_chunk_bytes(path), &a);
   a.counters = counters;
   a.width = width;
+  a.input_ready = (flags & PP_COUNT_INPUT_READY) ? 1 : 0;
   if (raw_frame) a.rot = 0;  // frame[i] as is: bit i mod 8 of bytes at address = i/8 mod 8
   cudaError_t e = pp::launch_count(a, path, di, st);
   if (e != cudaSuccess) return cuda_fail(e, "pp_count launch");
@@ -189,6 +191,12 @@ int pp_device_info(int device, int *num_sms, int *cc_major, int *cc_minor) {
 
 int pp_count(const void *data, size_t nbytes, int width, unsigned long long *counters,
              void *stream) {
+  return pp_count_ex(data, nbytes, width, counters, 0u, stream);
+}
+
+int pp_count_ex(const void *data, size_t nbytes, int width, unsigned long long *counters,
+                unsigned int flags, void *stream) {
+  if (flags & ~PP_COUNT_INPUT_READY) return fail(PP_EARG, "unknown pp_count_ex flags 0x%x", flags);
   if (!width_ok(width)) return fail(PP_EWIDTH, "word width must be one of (8, 16, 32, 64), got %d", width);
   if (nbytes % (size_t)(width / 8))
     return fail(PP_ELENGTH, "%zu bytes is not a multiple of the %d-byte word size", nbytes,
@@ -199,7 +207,8 @@ int pp_count(const void *data, size_t nbytes, int width, unsigned long long *cou
   if ((rc = check_device_ptr(data, "data"))) return rc;
   pp::DevInfo di;
   if ((rc = current_devinfo(&di))) return rc;
-  return count_device(data, nbytes, width, counters, static_cast<cudaStream_t>(stream), di);
+  return count_device(data, nbytes, width, counters, static_cast<cudaStream_t>(stream), di, false,
+                      flags);
 }
 
 int pp_count_frame(const void *data, size_t nbytes, unsigned long long *frame64,

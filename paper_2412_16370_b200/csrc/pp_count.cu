@@ -471,7 +471,7 @@ __device__ __forceinline__ uint64_t edge_load(const CountArgs &a, uint32_t lane)
   } else if (lane - 16 < a.tail_bytes / unit) {
     p = a.tail + unit * (lane - 16);
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // input complete (PDL)
+  if (!a.input_ready) asm volatile("griddepcontrol.wait;" ::: "memory");  // input complete (PDL)
   if (p && !PP_CHK_RANGE(p, unit, a.chk_lo, a.chk_hi)) p = nullptr;
   if (CB == 0) return p ? (uint64_t)__ldg(p) << frame_shift(p) : 0ull;
   if (!p) return 0xFFFFFFFFull;
@@ -546,8 +546,12 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       const uint64_t pol = policy_evict_first();
       // programmatic dependent launch: everything above overlapped the
       // previous grid's tail; its outputs (possibly our input) are complete
-      // and visible only after this wait
-      asm volatile("griddepcontrol.wait;" ::: "memory");
+      // and visible only after this wait.  With input_ready the caller
+      // vouches that the previous grid does not write the input: the copies
+      // start at once, and only the first ticket draw (the previous launch
+      // on this stream may share the ticket counter) waits.
+      bool waited = !a.input_ready;
+      if (waited) asm volatile("griddepcontrol.wait;" ::: "memory");
       PP_TL(1);
       uint32_t stage = 0, phase = 0;
       // chunk sequence: chunk blockIdx.x first, then either dynamic (ticket
@@ -572,8 +576,15 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         } else {  // checked build, failed check: no copy, the stage completes empty
           mbar_arrive(&full[stage]);
         }
-        ch = a.sched ? gridDim.x + (unsigned long long)(atomicAdd(a.sched, 1u) - a.sched_base)
-                     : ch + gridDim.x;
+        if (a.sched) {
+          if (!waited) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            waited = true;
+          }
+          ch = gridDim.x + (unsigned long long)(atomicAdd(a.sched, 1u) - a.sched_base);
+        } else {
+          ch += gridDim.x;
+        }
         if (++stage == Sh::kStages) {
           stage = 0;
           phase ^= 1;

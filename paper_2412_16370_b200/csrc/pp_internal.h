@@ -32,6 +32,11 @@ struct CountArgs {
   // slots exhausted)
   unsigned int *sched;
   unsigned int sched_base;
+  // PP_COUNT_INPUT_READY: the input is complete before the previous kernel on
+  // the stream starts (that kernel does not write it), so under programmatic
+  // dependent launch the loads need not wait for it; the ticket draws and the
+  // counter atomics still do
+  int input_ready;
   // checked builds (PP_CHECK_BOUNDS): the caller's byte range as the API
   // received it, and a per-launch {chunks consumed, CTAs finished} pair
   uintptr_t chk_lo, chk_hi;

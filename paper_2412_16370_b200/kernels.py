@@ -150,14 +150,19 @@ class B200Kernel:
     name = "b200"
     r = 128
 
-    def __init__(self, devices=None):
+    def __init__(self, devices=None, input_ready=False):
         """``devices``: host-resident inputs are split over these GPUs, one
         host link each (pp_count_host_multi); "all", a list of ordinals, or
         None (``POSPOPCNT_B200_DEVICES``, else the current device).  Device
-        inputs are always counted where they live."""
+        inputs are always counted where they live.  ``input_ready``: the
+        caller vouches that a CUDA input is not written by the kernel queued
+        before the count on its stream, so the count's loads may overlap that
+        kernel's tail (pp_count_ex, PP_COUNT_INPUT_READY); counter updates
+        still wait for it."""
         self.descriptor = KernelDescriptor(self.name, self.r, 2 * self.r)
         self._avail = None
         self.devices = devices
+        self.input_ready = bool(input_ready)
 
     def __repr__(self):
         return f"<kernel {self.name} r={self.r}>"
@@ -206,7 +211,11 @@ class B200Kernel:
             ptr = base.data_ptr() + view.offset
             dc = _device_counters(counters, w, dev)
             if dc is not None:
-                _lib.check(lib.pp_count(ptr, view.nbytes, w, dc.data_ptr(), stream))
+                if self.input_ready:
+                    _lib.check(lib.pp_count_ex(ptr, view.nbytes, w, dc.data_ptr(),
+                                               _lib.PP_COUNT_INPUT_READY, stream))
+                else:
+                    _lib.check(lib.pp_count(ptr, view.nbytes, w, dc.data_ptr(), stream))
                 return counters
             # host-side counters: count, copy back and synchronise in one C call
             vals = _host_result()
@@ -287,7 +296,7 @@ def select_kernel(override=None):
     return best
 
 
-def pospopcnt(data, width, counters=None, kernel=None, *, devices=None):
+def pospopcnt(data, width, counters=None, kernel=None, *, devices=None, input_ready=False):
     """Add the positional population count of ``data`` to ``counters``.
 
     Same contract as the reference (kernels.py:315-333): ``data`` is
@@ -297,11 +306,14 @@ def pospopcnt(data, width, counters=None, kernel=None, *, devices=None):
     ``kernel`` may be a kernel object, a kernel name, or None.
     ``devices`` (keyword only, an extension): split a HOST input over these
     GPUs ("all" or a list of ordinals), one host link each.
+    ``input_ready`` (keyword only, an extension): a CUDA input is not
+    written by the kernel queued just before this count on its stream, so
+    the count's loads may start while that kernel drains (B200Kernel).
     """
-    if devices is not None:
+    if devices is not None or input_ready:
         if kernel is not None and not (isinstance(kernel, str) and kernel == "b200"):
-            raise ValueError("devices= applies to the b200 kernel only")
-        kernel = B200Kernel(devices=devices)
+            raise ValueError("devices= / input_ready= apply to the b200 kernel only")
+        kernel = B200Kernel(devices=devices, input_ready=input_ready)
     check_width(width)
     view = InputView.of(data).check_complete(width)
     if counters is None:
@@ -362,8 +374,10 @@ def pospopcnt_all_widths(data, widths=None):
     return {w: fold_frame(frame, w, rot) for w in widths}
 
 
-def count_device(ptr, nbytes, width, counters_ptr, stream=0):
-    """Raw device-pointer entry (pp_count), for callers managing their own memory."""
+def count_device(ptr, nbytes, width, counters_ptr, stream=0, input_ready=False):
+    """Raw device-pointer entry (pp_count / pp_count_ex), for callers managing
+    their own memory."""
     lib = _lib.load()
-    _lib.check(lib.pp_count(ctypes.c_void_p(ptr), nbytes, width,
-                            ctypes.c_void_p(counters_ptr), ctypes.c_void_p(stream)))
+    _lib.check(lib.pp_count_ex(ctypes.c_void_p(ptr), nbytes, width, ctypes.c_void_p(counters_ptr),
+                               _lib.PP_COUNT_INPUT_READY if input_ready else 0,
+                               ctypes.c_void_p(stream)))

@@ -357,6 +357,46 @@ def test_pdl_contract_generate_then_count(cuda, oracle):
         assert [int(x) for x in ccnt[i].cpu()] == oracle.categories(oracle.gen_codes8(n, 2000 + i), 32)
 
 
+def test_input_ready_back_to_back(cuda, oracle):
+    """pp_count_ex(PP_COUNT_INPUT_READY): counts of inputs written before the
+    previous kernel on the stream may start loading during that kernel's
+    tail.  Back to back over distinct resident inputs (static and ticketed
+    chunk orders, unaligned views, alternating with plain counts into the
+    same counters): every count exact, counters accumulate.  Unknown flags
+    are an argument error."""
+    torch, pp = cuda
+    from paper_2412_16370_b200 import _lib, gen
+    from paper_2412_16370_b200.kernels import count_device
+    lib = _lib.load()
+    sizes = (2 << 20, 64 << 20, 256 << 20)  # static order / static / tickets
+    bufs = [gen.generate("uniform", n + 64, 3000 + i) for i, n in enumerate(sizes)]
+    torch.cuda.synchronize()
+    cnt = torch.zeros((len(sizes), 64), dtype=torch.int64, device="cuda")
+    sp = torch.cuda.current_stream().cuda_stream
+    reps = 6
+    for r in range(reps):
+        for i, (n, b) in enumerate(zip(sizes, bufs)):
+            off = (r * 5 + i) % 7
+            if r % 2:
+                count_device(b.data_ptr() + off, n, 64, cnt[i].data_ptr(), sp, input_ready=True)
+            else:
+                pp.pospopcnt(pp.InputView(b, off, n), 64, counters=cnt[i], input_ready=True)
+            _lib.check(lib.pp_count(b.data_ptr(), n, 64, cnt[i].data_ptr(), sp))
+    torch.cuda.synchronize()
+    for i, (n, b) in enumerate(zip(sizes, bufs)):
+        host = b.cpu().numpy()
+        want = [0] * 64
+        for r in range(reps):
+            off = (r * 5 + i) % 7
+            for j, v in enumerate(oracle.hs512(host, off, n, 64, threads=8)):
+                want[j] += v
+        for j, v in enumerate(oracle.hs512(host, 0, n, 64, threads=8)):
+            want[j] += reps * v
+        assert [int(x) for x in cnt[i].cpu()] == want, n
+    with pytest.raises(ValueError):
+        _lib.check(lib.pp_count_ex(bufs[0].data_ptr(), 64, 8, cnt[0].data_ptr(), 2, sp))
+
+
 def test_dynamic_schedule_boundaries_and_streams(cuda, oracle):
     """The ticketed chunk order (inputs >= 4096 chunks of 32 KiB = 128 MiB):
     lengths either side of the switch, odd offsets and tails, concurrent
