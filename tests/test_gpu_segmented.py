@@ -96,9 +96,8 @@ def test_ragged_random_segments_poison(cuda, oracle, rng, lanes):
         # the hybrid split over the same mixed lengths, with every lane hint:
         # G = 2 demotes to one lane per segment on CSR offsets, which must
         # drop the split (rows of long segments were never written)
-        if True:
-            hy = pp.pospopcnt_segmented(view, offs, w, lanes=lanes, hybrid=True)
-            assert np.array_equal(hy.cpu().numpy().view(np.uint64), want), w
+        hy = pp.pospopcnt_segmented(view, offs, w, lanes=lanes, hybrid=True)
+        assert np.array_equal(hy.cpu().numpy().view(np.uint64), want), w
         # accumulate semantics
         pp.pospopcnt_segmented(view, offs, w, out=out, lanes=lanes)
         assert np.array_equal(out.cpu().numpy().view(np.uint64), 2 * want), w
