@@ -1009,6 +1009,14 @@ def main_gpu(args):
         torch.cuda.empty_cache()
         strong_c5 = run_strong_c5(args, lib, world, rank, dev, st, use_dist, peers)
 
+    # the other BASELINE configs as one summary each, measured in this run
+    # (one child bench.py per config, after this config's own timing)
+    others = None
+    if args.all_configs and cfg == "c2" and not use_dist and args.width in (0, 8):
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        others = run_other_configs(args)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
@@ -1046,6 +1054,7 @@ def main_gpu(args):
             "exact": exact,
             "per_width_gbs": per_width,
             "c4_short_sweep": c4_sweep,
+            "other_configs": others,
         }
         emit(line)
     if peers is not None:
@@ -1054,6 +1063,41 @@ def main_gpu(args):
     if use_dist:
         dist.destroy_process_group()
     return 0
+
+
+OTHER_CONFIGS = ("c1", "c3", "c4", "c4seg", "c3cat")
+
+
+def run_other_configs(args):
+    """One child `bench.py --config X` per other BASELINE config (same GPU,
+    same K/W, no e2e / CPU legs); returns {config: summary of its line}."""
+    out = {}
+    for cfg in OTHER_CONFIGS:
+        cmd = [sys.executable, os.path.abspath(__file__), "--config", cfg,
+               "--steps", str(args.steps), "--warmup", str(args.warmup), "--no-e2e",
+               "--no-cpu-baseline", "--no-strong-c5", "--no-all-configs"]
+        if not args.input_ready:
+            cmd.append("--no-input-ready")
+        t0 = time.time()
+        try:
+            res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+            lines = [x for x in res.stdout.splitlines() if x.strip().startswith("{")]
+            if res.returncode != 0 or not lines:
+                out[cfg] = {"error": f"rc={res.returncode}: {res.stderr.strip()[-300:]}"}
+                continue
+            d = json.loads(lines[-1])
+        except Exception as exc:  # noqa: BLE001 - recorded, the headline stands
+            out[cfg] = {"error": repr(exc)[:300]}
+            continue
+        r = d.get("roofline") or {}
+        out[cfg] = {"workload": d["config"]["workload"], "value": d["value"], "unit": d["unit"],
+                    "ms_per_step": d["ms_per_step"], "exact": d.get("exact"),
+                    "roofline": {k: r.get(k) for k in ("bound", "achieved", "peak", "unit",
+                                                       "frac", "kernel")},
+                    "timing": d.get("timing"), "cold_call": d.get("cold_call"),
+                    "launch": d.get("launch"), "clocks": d.get("clocks"),
+                    "wall_s": round(time.time() - t0, 1)}
+    return out
 
 
 _JSON_OUT = None  # the real stdout: the one JSON line goes here, nothing else
@@ -1121,6 +1165,8 @@ def main():
     ap.add_argument("--cpu-min-time", type=float, default=5.0)
     ap.add_argument("--no-input-ready", dest="input_ready", action="store_false",
                     help="count with plain pp_count (loads wait for the previous kernel)")
+    ap.add_argument("--no-all-configs", dest="all_configs", action="store_false",
+                    help="skip the other BASELINE configs' summaries in the c2 line")
     ap.add_argument("--no-strong-c5", dest="strong_c5", action="store_false",
                     help="skip the C5 strong-scaling object of the c2 line")
     args = ap.parse_args()

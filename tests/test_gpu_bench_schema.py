@@ -53,12 +53,20 @@ def test_bench_line_contract(cuda):
     assert d["gpu_launches"] == 5
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert "workload" in d["config"]
+    # every other BASELINE config measured in the same run, each exact
+    oc = d["other_configs"]
+    assert set(oc) == {"c1", "c3", "c4", "c4seg", "c3cat"}, oc
+    for name, o in oc.items():
+        assert "error" not in o, (name, o)
+        assert o["exact"] is True and o["value"] > 0, (name, o)
+    assert oc["c3cat"]["roofline"]["bound"] == "alu"
+    assert oc["c1"]["cold_call"]["us_median"] > 0
 
 
 def test_reference_arm_contract():
     d = _run("--impl", "reference", "--steps", "1", "--warmup", "3")
     g = _run("--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu-baseline",
-             "--no-strong-c5")
+             "--no-strong-c5", "--no-all-configs")
     # same workload description as the GPU arm: the driver matches the lines
     assert d["config"] == g["config"] and d["metric"] == g["metric"]
     assert d["scaling"] == g["scaling"] == "weak"
