@@ -455,10 +455,6 @@ def run_strong_c5(args, lib, world, rank, dev, st, use_dist, peers):
     return {"value": round(gbs, 1), "unit": "GB/s", "ms_per_step": round(t_ms / steps, 4),
             "steps": steps, "warmup": warm, "n_gpus": world, "scaling": "strong",
             "bytes_total": total, "bytes_per_gpu": n,
-            "launch": ("pp_count_ex(..., PP_COUNT_INPUT_READY): inputs written once before "
-                       "the first count, so a step's loads may overlap the previous step's tail"
-                       if count_flags and not categorical and seg_out is None and not fused
-                       else "plain launches"),
             "exchange": ("fused in-kernel peer adds" if fused else
                          "NCCL allreduce per step" if use_dist else "none (one GPU)"),
             "hbm_frac_per_gpu": round(gbs / world / load_peaks()[0], 4),
@@ -1026,6 +1022,10 @@ def main_gpu(args):
             "dtype": "u8" if w == 8 else f"u{w}",
             "data": "synthetic: seeded splitmix64 generators, generated in place in HBM",
             "config": config_dict(cfg, world, per_step_bytes, job_bytes, w),
+            "launch": ("pp_count_ex(..., PP_COUNT_INPUT_READY): inputs written once before "
+                       "the first count, so a step's loads may overlap the previous step's tail"
+                       if count_flags and not categorical and seg_out is None and not fused
+                       else "plain launches"),
             "exchange": ("none (rows stay on their rank)" if seg_out is not None else
                          "fused: the counting kernel adds into every rank's IPC-mapped "
                          "counters (pp_count_multi)" if fused else
