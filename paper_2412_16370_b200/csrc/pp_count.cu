@@ -558,6 +558,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       // t of a shared counter = chunk gridDim.x + t, so every CTA finishes
       // within about one chunk of the others) or the static grid stride
       unsigned long long ch = blockIdx.x;
+      uint32_t issued = 0;  // chunks this CTA has issued
       for (;;) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (ch >= nchunks) {  // tell the consumers to stop: no bytes, one arrival
@@ -576,12 +577,17 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         } else {  // checked build, failed check: no copy, the stage completes empty
           mbar_arrive(&full[stage]);
         }
-        if (a.sched) {
+        // the first a.lead chunks of every CTA are static (blockIdx.x +
+        // j * gridDim.x): a whole ring's worth can be issued before the
+        // first ticket, i.e. (with input_ready) while the previous launch on
+        // the stream still drains; tickets number the chunks after those
+        if (a.sched && ++issued >= a.lead) {
           if (!waited) {
             asm volatile("griddepcontrol.wait;" ::: "memory");
             waited = true;
           }
-          ch = gridDim.x + (unsigned long long)(atomicAdd(a.sched, 1u) - a.sched_base);
+          ch = (unsigned long long)a.lead * gridDim.x +
+               (unsigned long long)(atomicAdd(a.sched, 1u) - a.sched_base);
         } else {
           ch += gridDim.x;
         }
@@ -998,19 +1004,29 @@ void sched_commit(cudaStream_t st) {
 template <typename Kern>
 static cudaError_t launch_tma(Kern kernel, unsigned grid, unsigned block, size_t smem,
                               cudaStream_t st, const CountArgs &a0, unsigned long long *sink,
-                              bool want_pdl, const DevInfo &di) {
+                              bool want_pdl, const DevInfo &di, unsigned stages) {
   static const bool pdl_off = std::getenv("PP_NO_PDL") != nullptr;
+  static const int lead_env = [] {
+    const char *e = std::getenv("PP_STATIC_LEAD");  // A/B: static chunks per CTA before tickets
+    return e ? std::atoi(e) : 0;
+  }();
   const bool pdl = want_pdl && !pdl_off;
   CountArgs a = a0;
+  a.lead = lead_env > 0 ? (unsigned)lead_env : stages;
+  // every CTA's first `lead` chunks are static; tickets cover the rest, plus
+  // one failing draw per CTA: the launch consumes exactly `units` tickets
+  const unsigned long long static_chunks = (unsigned long long)a.lead * grid;
+  const unsigned long long units =
+      a.nchunks > static_chunks ? a.nchunks - static_chunks + grid : 0;
   // the dynamic order pays off once a CTA streams tens of chunks (+6 % at
   // 256 MiB, +2 % at 1 GiB); below that the static order has no tail to
   // even out and saves the slot lookup (scripts/pdl_sweep.py).  The slot's
   // base and the launch are one critical section: launches on a stream must
   // reach it in the order their bases were handed out.
   std::unique_lock<std::mutex> lk;
-  if (a.nchunks >= kDynMinChunks) {
+  if (a.nchunks >= kDynMinChunks && units > 0) {
     lk = sched_lock();
-    a.sched = sched_slot(di, st, a.nchunks, &a.sched_base);
+    a.sched = sched_slot(di, st, units, &a.sched_base);
   }
 #if PP_CHECK_BOUNDS
   // per-launch {chunks consumed, CTAs finished} (stream-ordered scratch)
@@ -1039,7 +1055,7 @@ static cudaError_t launch_tma(Kern kernel, unsigned grid, unsigned block, size_t
 #endif
   if (a.sched) {
     if (e != cudaSuccess)
-      sched_rollback(a.nchunks);
+      sched_rollback(units);
     else
       sched_commit(st);
   }
@@ -1051,7 +1067,7 @@ cudaError_t launch_count(const CountArgs &a, LoadPath path, const DevInfo &di,
   if (path == LoadPath::kTma) {
     const unsigned g = grid_for(a.nchunks, (unsigned long long)di.count_sms);
     cudaError_t e = launch_tma(pp_tma_kernel<1>, g, kTmaThreads, kTmaSmemBytes, st, a, nullptr,
-                               a.body_bytes < pdl_max_body(), di);
+                               a.body_bytes < pdl_max_body(), di, kTmaStages);
     if (e != cudaSuccess) return e;
   } else {
     const unsigned g =
@@ -1067,16 +1083,16 @@ static cudaError_t launch_codes(const CountArgs &a, const DevInfo &di, cudaStrea
   switch (a.width) {
     case 8:
       return launch_tma(pp_tma_kernel<8, PP_CAT_NCW, CB>, g, CatShape::kThreads, CatShape::kSmem,
-                        st, a, nullptr, true, di);
+                        st, a, nullptr, true, di, CatShape::kStages);
     case 16:
       return launch_tma(pp_tma_kernel<16, PP_CAT_NCW, CB>, g, CatShape::kThreads,
-                        CatShape::kSmem, st, a, nullptr, true, di);
+                        CatShape::kSmem, st, a, nullptr, true, di, CatShape::kStages);
     case 32:
       return launch_tma(pp_tma_kernel<32, PP_CAT_NCW, CB>, g, CatShape::kThreads,
-                        CatShape::kSmem, st, a, nullptr, true, di);
+                        CatShape::kSmem, st, a, nullptr, true, di, CatShape::kStages);
     default:
       return launch_tma(pp_tma_kernel<64, PP_CAT_NCW, CB>, g, CatShape::kThreads,
-                        CatShape::kSmem, st, a, nullptr, true, di);
+                        CatShape::kSmem, st, a, nullptr, true, di, CatShape::kStages);
   }
 }
 
@@ -1091,7 +1107,7 @@ cudaError_t launch_readonly(const CountArgs &a, unsigned long long *sink, const 
                             cudaStream_t st) {
   const unsigned g = grid_for(a.nchunks, (unsigned long long)di.count_sms);
   return launch_tma(pp_tma_kernel<0>, g, kTmaThreads, kTmaSmemBytes, st, a, sink,
-                    a.body_bytes < pdl_max_body(), di);
+                    a.body_bytes < pdl_max_body(), di, kTmaStages);
 }
 
 cudaError_t chk_read_count(ChkRecHost *out, bool reset) {

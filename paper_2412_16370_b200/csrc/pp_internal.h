@@ -37,6 +37,8 @@ struct CountArgs {
   // dependent launch the loads need not wait for it; the ticket draws and the
   // counter atomics still do
   int input_ready;
+  // static chunks per CTA before its first ticket (launch_tma: the ring depth)
+  unsigned int lead;
   // checked builds (PP_CHECK_BOUNDS): the caller's byte range as the API
   // received it, and a per-launch {chunks consumed, CTAs finished} pair
   uintptr_t chk_lo, chk_hi;
