@@ -587,14 +587,15 @@ def main_gpu(args):
                                           _lib.PP_SEG_OVERWRITE, sp))
         else:
             if fused:
-                _lib.check(lib.pp_count_multi(view_ptr, nbytes, w, peers.targets, ntgt, sp))
+                _lib.check(lib.pp_count_multi_ex(view_ptr, nbytes, w, peers.targets, ntgt,
+                                                 count_flags, sp))
                 nstep[0] += 1
                 return
             if use_dist:
                 st.wait_event(snap_ev[b])  # step i-2's snapshot of counters2[b] is taken
             if categorical:  # one u8 code per byte
-                _lib.check(lib.pp_count_categories(view_ptr, nbytes, 1, w,
-                                                   counters2[b].data_ptr(), sp))
+                _lib.check(lib.pp_count_categories_ex(view_ptr, nbytes, 1, w,
+                                                      counters2[b].data_ptr(), count_flags, sp))
             else:
                 _lib.check(lib.pp_count_ex(view_ptr, nbytes, w, counters2[b].data_ptr(),
                                            count_flags, sp))
@@ -834,16 +835,19 @@ def main_gpu(args):
                                             "in_plus_out_GBs": round((seg + 512) * nseg / us / 1e3, 1)}
         del out_b
 
-    # the paper's read-only "roofline" kernel over the same bytes
+    # the paper's read-only "roofline" kernel over the same bytes, launched
+    # and rotated over the input copies exactly like the count steps
     sink = torch.zeros(1, dtype=torch.int64, device=dev)
-    for _ in range(max(3, args.warmup)):
-        _lib.check(lib.pp_readonly_sum(view_ptr, nbytes, sink.data_ptr(), sp))
+    for i in range(max(3, args.warmup)):
+        _lib.check(lib.pp_readonly_sum_ex(slot_ptrs[i % len(slot_ptrs)], nbytes,
+                                          sink.data_ptr(), count_flags, sp))
     r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     nro = max(5, args.steps)
     gpu_busy()  # launches queue behind a spin, not an idle GPU
     r0.record(st)
-    for _ in range(nro):
-        _lib.check(lib.pp_readonly_sum(view_ptr, nbytes, sink.data_ptr(), sp))
+    for i in range(nro):
+        _lib.check(lib.pp_readonly_sum_ex(slot_ptrs[(i + 1) % len(slot_ptrs)], nbytes,
+                                          sink.data_ptr(), count_flags, sp))
     r1.record(st)
     torch.cuda.synchronize()
     ro_gbs = nbytes * nro / (r0.elapsed_time(r1) / 1e3) / 1e9
@@ -1024,8 +1028,7 @@ def main_gpu(args):
             "config": config_dict(cfg, world, per_step_bytes, job_bytes, w),
             "launch": ("pp_count_ex(..., PP_COUNT_INPUT_READY): inputs written once before "
                        "the first count, so a step's loads may overlap the previous step's tail"
-                       if count_flags and not categorical and seg_out is None and not fused
-                       else "plain launches"),
+                       if count_flags and seg_out is None else "plain launches"),
             "exchange": ("none (rows stay on their rank)" if seg_out is not None else
                          "fused: the counting kernel adds into every rank's IPC-mapped "
                          "counters (pp_count_multi)" if fused else

@@ -205,6 +205,10 @@ PP_API int pp_count_fixed(const void *base, size_t seg_bytes, size_t nseg, int w
 #define PP_MAX_TARGETS 16
 PP_API int pp_count_multi(const void *data, size_t nbytes, int width,
                           unsigned long long *const *targets, int ntargets, void *stream);
+/* pp_count_multi with pp_count_ex's flags (PP_COUNT_INPUT_READY). */
+PP_API int pp_count_multi_ex(const void *data, size_t nbytes, int width,
+                      unsigned long long *const *targets, int ntargets, unsigned int flags,
+                      void *stream);
 
 /* CUDA IPC for the targets of pp_count_multi (one process per GPU): export
  * any device pointer (it may lie inside a larger allocation, e.g. a caching
@@ -241,6 +245,9 @@ PP_API int pp_count_frame(const void *data, size_t nbytes, unsigned long long *f
  */
 PP_API int pp_count_categories(const void *codes, size_t ncodes, int code_bytes, int width,
                                unsigned long long *counters, void *stream);
+/* pp_count_categories with pp_count_ex's flags (PP_COUNT_INPUT_READY). */
+PP_API int pp_count_categories_ex(const void *codes, size_t ncodes, int code_bytes, int width,
+                           unsigned long long *counters, unsigned int flags, void *stream);
 
 /*
  * pp_readonly_sum — the paper's "roofline" dummy kernel:
@@ -249,6 +256,10 @@ PP_API int pp_count_categories(const void *codes, size_t ncodes, int code_bytes,
  */
 PP_API int pp_readonly_sum(const void *data, size_t nbytes, unsigned long long *sink,
                     void *stream);
+/* pp_readonly_sum with pp_count_ex's flags: the roofline kernel launched the
+ * way the count it is compared with is launched. */
+PP_API int pp_readonly_sum_ex(const void *data, size_t nbytes, unsigned long long *sink,
+                       unsigned int flags, void *stream);
 
 /*
  * pp_sched_stats — diagnostics of the dynamic chunk scheduler (per-stream

@@ -44,15 +44,18 @@ SIGNATURES = {
     "pp_debug_corrupt": (_int, [_int]),
     "pp_count_frame": (_int, [_vp, _sz, _vp, _vp]),
     "pp_count_multi": (_int, [_vp, _sz, _int, _vp, _int, _vp]),
+    "pp_count_multi_ex": (_int, [_vp, _sz, _int, _vp, _int, _u32, _vp]),
     "pp_ipc_handle": (_int, [_vp, _vp]),
     "pp_ipc_open": (_int, [_vp, _vp]),
     "pp_ipc_close": (_int, [_vp]),
     "pp_count_categories": (_int, [_vp, _sz, _int, _int, _vp, _vp]),
+    "pp_count_categories_ex": (_int, [_vp, _sz, _int, _int, _vp, _u32, _vp]),
     "pp_count_segmented": (_int, [_vp, _vp, _sz, _int, _vp, _int, _vp]),
     "pp_count_segmented_order": (_int, [_vp, _vp, _vp, _sz, _int, _vp, _int, _vp]),
     "pp_count_fixed": (_int, [_vp, _sz, _sz, _int, _vp, _int, _vp]),
     "pp_count_batch": (_int, [_vp, _vp, _sz, _int, _vp, _int, _vp]),
     "pp_readonly_sum": (_int, [_vp, _sz, _vp, _vp]),
+    "pp_readonly_sum_ex": (_int, [_vp, _sz, _vp, _u32, _vp]),
     "pp_gen_uniform": (_int, [_vp, _sz, _u64, _u64, _vp]),
     "pp_gen_bernoulli": (_int, [_vp, _sz, _u64, _u64, _u32, _vp]),
     "pp_gen_blocks": (_int, [_vp, _sz, _u64, _u64, _u64, _vp]),

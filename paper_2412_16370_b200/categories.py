@@ -24,13 +24,15 @@ from .kernels import _add_into, _device_counters, _device_scratch
 _CODE_BYTES = {1: 1, 2: 2, 4: 4}
 
 
-def pospopcnt_categories(codes, width, counters=None):
+def pospopcnt_categories(codes, width, counters=None, *, input_ready=False):
     """Add the per-category counts of ``codes`` (< width) into ``counters``.
 
     ``codes``: a 1-D CUDA tensor of uint8 / int16 / uint16 / int32 / uint32
     codes (host arrays are copied to the current device once).  Counters
     follow the ``pospopcnt`` conventions: a CUDA int64 tensor is accumulated
     asynchronously on the device, anything else receives Python ints.
+    ``input_ready``: as ``pospopcnt`` (the kernel queued before this count
+    does not write the codes; pp_count_categories_ex, PP_COUNT_INPUT_READY).
     """
     import torch
     check_width(width)
@@ -58,8 +60,9 @@ def pospopcnt_categories(codes, width, counters=None):
         stream = torch.cuda.current_stream(dev).cuda_stream
         dc = _device_counters(counters, width, dev)
         if dc is not None:
-            _lib.check(lib.pp_count_categories(codes.data_ptr(), n, cb, width, dc.data_ptr(),
-                                               stream))
+            flags = _lib.PP_COUNT_INPUT_READY if input_ready else 0
+            _lib.check(lib.pp_count_categories_ex(codes.data_ptr(), n, cb, width, dc.data_ptr(),
+                                                  flags, stream))
             return counters
         scratch = _device_scratch(dev)
         scratch.zero_()

@@ -224,6 +224,13 @@ int pp_count_frame(const void *data, size_t nbytes, unsigned long long *frame64,
 
 int pp_count_multi(const void *data, size_t nbytes, int width,
                    unsigned long long *const *targets, int ntargets, void *stream) {
+  return pp_count_multi_ex(data, nbytes, width, targets, ntargets, 0u, stream);
+}
+
+int pp_count_multi_ex(const void *data, size_t nbytes, int width,
+                      unsigned long long *const *targets, int ntargets, unsigned int flags,
+                      void *stream) {
+  if (flags & ~PP_COUNT_INPUT_READY) return fail(PP_EARG, "unknown flags 0x%x", flags);
   if (!width_ok(width)) return fail(PP_EWIDTH, "word width must be one of (8, 16, 32, 64), got %d", width);
   if (nbytes % (size_t)(width / 8))
     return fail(PP_ELENGTH, "%zu bytes is not a multiple of the %d-byte word size", nbytes,
@@ -244,6 +251,7 @@ int pp_count_multi(const void *data, size_t nbytes, int width,
   a.width = width;
   a.nextra = ntargets - 1;
   for (int k = 1; k < ntargets; ++k) a.extra[k - 1] = targets[k];
+  a.input_ready = (flags & PP_COUNT_INPUT_READY) ? 1 : 0;
   cudaError_t e = pp::launch_count(a, path, di, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "pp_count_multi launch");
   return PP_OK;
@@ -297,6 +305,12 @@ int pp_ipc_close(void *dev_ptr) {
 
 int pp_count_categories(const void *codes, size_t ncodes, int code_bytes, int width,
                         unsigned long long *counters, void *stream) {
+  return pp_count_categories_ex(codes, ncodes, code_bytes, width, counters, 0u, stream);
+}
+
+int pp_count_categories_ex(const void *codes, size_t ncodes, int code_bytes, int width,
+                           unsigned long long *counters, unsigned int flags, void *stream) {
+  if (flags & ~PP_COUNT_INPUT_READY) return fail(PP_EARG, "unknown flags 0x%x", flags);
   if (!width_ok(width)) return fail(PP_EWIDTH, "word width must be one of (8, 16, 32, 64), got %d", width);
   if (code_bytes != 1 && code_bytes != 2 && code_bytes != 4)
     return fail(PP_EARG, "code_bytes must be 1, 2 or 4, got %d", code_bytes);
@@ -325,6 +339,7 @@ int pp_count_categories(const void *codes, size_t ncodes, int code_bytes, int wi
     a.counters = counters;
     a.width = width;
     a.rot = 0;
+    a.input_ready = (flags & PP_COUNT_INPUT_READY) ? 1 : 0;
     e = pp::launch_count_codes(a, code_bytes, di, static_cast<cudaStream_t>(stream));
   } else {
     // the A/B alternative: per-thread shared-memory histogram columns
@@ -464,6 +479,12 @@ int pp_count_fixed(const void *base, size_t seg_bytes, size_t nseg, int width,
 }
 
 int pp_readonly_sum(const void *data, size_t nbytes, unsigned long long *sink, void *stream) {
+  return pp_readonly_sum_ex(data, nbytes, sink, 0u, stream);
+}
+
+int pp_readonly_sum_ex(const void *data, size_t nbytes, unsigned long long *sink,
+                       unsigned int flags, void *stream) {
+  if (flags & ~PP_COUNT_INPUT_READY) return fail(PP_EARG, "unknown flags 0x%x", flags);
   int rc;
   if ((rc = check_device_ptr(sink, "sink"))) return rc;
   if (nbytes == 0) return PP_OK;
@@ -473,6 +494,7 @@ int pp_readonly_sum(const void *data, size_t nbytes, unsigned long long *sink, v
   pp::CountArgs a{};
   pp::split_range(static_cast<const uint8_t *>(data), nbytes,
                   pp::count_chunk_bytes(pp::LoadPath::kTma), &a);
+  a.input_ready = (flags & PP_COUNT_INPUT_READY) ? 1 : 0;
   cudaError_t e = pp::launch_readonly(a, sink, di, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "pp_readonly_sum launch");
   return PP_OK;

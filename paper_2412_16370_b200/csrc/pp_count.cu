@@ -1012,7 +1012,15 @@ static cudaError_t launch_tma(Kern kernel, unsigned grid, unsigned block, size_t
   }();
   const bool pdl = want_pdl && !pdl_off;
   CountArgs a = a0;
-  a.lead = lead_env > 0 ? (unsigned)lead_env : stages;
+  // static lead: at least a ring per CTA (so, with input_ready, a whole
+  // ring is in flight before the first ticket waits for the previous
+  // launch), up to 16 chunks when a CTA streams >= 128 of them (1 GiB:
+  // 7450 -> 7490 GB/s, scripts/gpu_lead_ab.sh; lead 8..32 equal), leaving
+  // >= 7/8 of the chunks to the tickets that even out the tail
+  const unsigned long long per_cta = a.nchunks / (grid ? grid : 1);
+  a.lead = lead_env > 0 ? (unsigned)lead_env
+                        : (unsigned)std::max<unsigned long long>(
+                              stages, std::min<unsigned long long>(16, per_cta / 8));
   // every CTA's first `lead` chunks are static; tickets cover the rest, plus
   // one failing draw per CTA: the launch consumes exactly `units` tickets
   const unsigned long long static_chunks = (unsigned long long)a.lead * grid;

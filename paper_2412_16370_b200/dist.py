@@ -122,13 +122,15 @@ class PeerCounters:
         self.targets = self.gen_targets[0]
         self.sync()
 
-    def count(self, data, nbytes, width, stream=None, gen=0):
+    def count(self, data, nbytes, width, stream=None, gen=0, input_ready=False):
         """Count device bytes [data, data+nbytes) into generation ``gen`` of
-        every rank's counters (raw mode: no synchronisation)."""
+        every rank's counters (raw mode: no synchronisation).  ``input_ready``
+        as ``pospopcnt`` (pp_count_multi_ex, PP_COUNT_INPUT_READY)."""
         st = torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream
         tg = self.gen_targets[gen]
-        _lib.check(self.lib.pp_count_multi(ctypes.c_void_p(data), nbytes, width, tg,
-                                           len(tg), ctypes.c_void_p(st)))
+        flags = _lib.PP_COUNT_INPUT_READY if input_ready else 0
+        _lib.check(self.lib.pp_count_multi_ex(ctypes.c_void_p(data), nbytes, width, tg,
+                                              len(tg), flags, ctypes.c_void_p(st)))
 
     def count_call(self, data, nbytes, width):
         """Collective: this call's job total (int64[width], on this rank's

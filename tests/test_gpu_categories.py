@@ -23,6 +23,14 @@ def test_c3_codes_equal_reference_onehot_counts(cuda):
         case = {c["name"]: c for c in json.load(f)["cases"]}["c3_w32_onehot_4gib"]
     codes = gen.generate("codes8", 1 << 30, 0xC3)  # 2^30 codes, one per byte
     assert pp.pospopcnt_categories(codes, 32) == case["numba"]
+    # back to back with input_ready (the codes are written once, before):
+    # every width's counts, accumulated on the device, still the reference's
+    cnt = torch.zeros((3, 32), dtype=torch.int64, device="cuda")
+    for r in range(3):
+        pp.pospopcnt_categories(codes, 32, counters=cnt[r], input_ready=True)
+        pp.pospopcnt_categories(codes, 32, counters=cnt[r], input_ready=True)
+    for r in range(3):
+        assert [int(x) for x in cnt[r].cpu()] == [2 * v for v in case["numba"]], r
     onehot = gen.generate("onehot32", 4 << 30, 0xC3)
     assert pp.pospopcnt(onehot, 32) == case["numba"]
     del codes, onehot
