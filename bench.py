@@ -837,17 +837,20 @@ def main_gpu(args):
 
     # the paper's read-only "roofline" kernel over the same bytes, launched
     # and rotated over the input copies exactly like the count steps
+    # (starting half a rotation away from the copies the timed steps read)
     sink = torch.zeros(1, dtype=torch.int64, device=dev)
+    nslots = len(slot_ptrs)
+    s0 = args.warmup + args.steps + nslots // 2
     for i in range(max(3, args.warmup)):
-        _lib.check(lib.pp_readonly_sum_ex(slot_ptrs[i % len(slot_ptrs)], nbytes,
+        _lib.check(lib.pp_readonly_sum_ex(slot_ptrs[(s0 + i) % nslots], nbytes,
                                           sink.data_ptr(), count_flags, sp))
     r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     nro = max(5, args.steps)
     gpu_busy()  # launches queue behind a spin, not an idle GPU
     r0.record(st)
     for i in range(nro):
-        _lib.check(lib.pp_readonly_sum_ex(slot_ptrs[(i + 1) % len(slot_ptrs)], nbytes,
-                                          sink.data_ptr(), count_flags, sp))
+        _lib.check(lib.pp_readonly_sum_ex(slot_ptrs[(s0 + max(3, args.warmup) + i) % nslots],
+                                          nbytes, sink.data_ptr(), count_flags, sp))
     r1.record(st)
     torch.cuda.synchronize()
     ro_gbs = nbytes * nro / (r0.elapsed_time(r1) / 1e3) / 1e9
