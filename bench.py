@@ -901,7 +901,19 @@ def main_gpu(args):
         pinned.copy_(buf[offset:offset + nbytes])
         torch.cuda.synchronize()
         nst = max(2, min(args.steps, 5))
-        api = pp.pospopcnt_categories if categorical else pp.pospopcnt
+        if use_dist and not categorical:
+            # the job's public call at N ranks: every rank's host-resident
+            # shard through its own link (pp_count_host), the w counters
+            # all-reduced over the process group, the total read back
+            from paper_2412_16370_b200.dist import pospopcnt_sharded
+            api = lambda data, width: pospopcnt_sharded(data, width).cpu()  # noqa: E731
+            e2e_path = ("pospopcnt_sharded(pinned host shard) on every rank: pp_count_host "
+                        "(64 MiB chunks, H2D on a copy stream overlapped with counting), the "
+                        "counters all-reduced over NCCL and read back")
+        else:
+            api = pp.pospopcnt_categories if categorical else pp.pospopcnt
+            e2e_path = ("pospopcnt(pinned host tensor) -> pp_count_host: 64 MiB chunks, "
+                        "H2D on a copy stream overlapped with counting")
         for _ in range(1):
             api(pinned, w)
         if use_dist:
@@ -916,9 +928,7 @@ def main_gpu(args):
             t_e2e = tt.item()
         e2e = {"value": round(world * nbytes * nst / t_e2e / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": w * 8,
-               "path": "pospopcnt(pinned host tensor) -> pp_count_host: 64 MiB chunks, "
-                       "H2D on a copy stream overlapped with counting",
-               "steps": nst}
+               "path": e2e_path, "steps": nst}
         del pinned, res
     elif args.e2e and seg_out is not None:
         # segmented batch from host memory through the public API: the batch

@@ -59,7 +59,7 @@ def test_bench_gpus_flag_relaunches_ranks(cuda):
     (same command shape as the driver's) and reports n_gpus = 2."""
     env = dict(os.environ, PP_BENCH_DEVICE="0", PP_BENCH_BACKEND="gloo")
     cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3",
-           "--warmup", "3", "--no-e2e", "--no-cpu-baseline"]
+           "--warmup", "3", "--no-cpu-baseline"]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     out = [x for x in res.stdout.splitlines() if x.strip()]
@@ -67,6 +67,9 @@ def test_bench_gpus_flag_relaunches_ranks(cuda):
     line = json.loads(out[0])
     assert line["n_gpus"] == 2 and line["exact"] is True and line["strong_c5"]["exact"] is True
     assert line["config"]["bytes_per_step_all_gpus"] == 2 << 30
+    # e2e at N ranks: every rank's host shard through pospopcnt_sharded
+    e = line["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == 1 << 30 and "sharded" in e["path"]
 
 
 def test_bench_gpus_mismatch_fails_loudly(cuda):
