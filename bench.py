@@ -526,18 +526,22 @@ def main_gpu(args):
         first_word = rank * alloc // word_unit
     buf = gen.generate(kind, alloc, seed, device=dev, word_offset=first_word, q=655)
     view_ptr = buf.data_ptr() + offset
-    # inputs that fit in the 126 MB L2 (C1, C4): R identical copies in R
-    # slots of one >= 512 MiB buffer, step i counting slot i mod R, so the
-    # steps run back to back and every step's input was last touched
-    # R - 1 steps (>= 510 MiB of other inputs) earlier: cold in L2 without a
-    # flush between steps.  The flush-then-one-launch protocol is reported
-    # beside it as the cold single-call latency.
+    # R identical copies of the input in R slots of one buffer, step i
+    # counting slot i mod R, steps back to back: every step's input was last
+    # touched R - 1 steps (>= 510 MiB and >= 2 other inputs) earlier, so it
+    # is cold in L2 without a flush between steps -- also when consecutive
+    # launches overlap (the next count's loads start during this one,
+    # INPUT_READY + the trigger at kernel start: two launches over ONE
+    # buffer would share L2 lines).  C5 (one 64 GiB array) keeps one copy:
+    # overlapping launches read it 64 GiB apart.  For inputs that fit in L2
+    # (C1, C4) the flush-then-one-launch protocol is reported beside it as
+    # the cold single-call latency.
     small = nbytes < L2_FLUSH_BELOW
     rot = None
     slot_ptrs = [view_ptr]
-    if small:
+    if not strong and (cfg != "c4seg" or small):
         slot = (alloc + 4095) // 4096 * 4096  # keeps the view's address mod 4096
-        nslot = max(2, -(-L2_FLUSH_BYTES // slot))
+        nslot = max(3, -(-L2_FLUSH_BYTES // slot))
         rot = torch.empty(nslot * slot, dtype=torch.uint8, device=dev)
         rot.view(nslot, slot)[:, :alloc].copy_(buf.view(1, alloc).expand(nslot, alloc))
         slot_ptrs = [rot.data_ptr() + i * slot + offset for i in range(nslot)]
@@ -778,13 +782,16 @@ def main_gpu(args):
         for ww in (8, 16, 32, 64):
             if nbytes % (ww // 8):
                 continue
-            for _ in range(2):
-                _lib.check(lib.pp_count(view_ptr, nbytes, ww, scratch_w.data_ptr(), sp))
+            ns = len(slot_ptrs)
+            for i in range(2):
+                _lib.check(lib.pp_count_ex(slot_ptrs[i % ns], nbytes, ww, scratch_w.data_ptr(),
+                                           count_flags, sp))
             q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             gpu_busy()  # launches queue behind a spin, not an idle GPU
             q0.record(st)
-            for _ in range(args.steps):
-                _lib.check(lib.pp_count(view_ptr, nbytes, ww, scratch_w.data_ptr(), sp))
+            for i in range(args.steps):
+                _lib.check(lib.pp_count_ex(slot_ptrs[(2 + i) % ns], nbytes, ww,
+                                           scratch_w.data_ptr(), count_flags, sp))
             q1.record(st)
             torch.cuda.synchronize()
             per_width[str(ww)] = round(nbytes * args.steps / (q0.elapsed_time(q1) / 1e3) / 1e9, 1)
@@ -1049,10 +1056,11 @@ def main_gpu(args):
                          "stream") if world > 1 else "none (one GPU)",
             "timing": {"settle": f"{n_settle + 1} untimed launches (>= {SETTLE_MS:.0f} ms) "
                                  "after the warm-up steps, into scratch counters",
-                       "l2": "input >> 126 MB L2, no flush needed" if not small
-                             else f"inputs larger than L2: {len(slot_ptrs)} copies of the input "
-                                  f"({len(slot_ptrs) * nbytes >> 20} MiB), step i counts copy "
-                                  f"i mod {len(slot_ptrs)}, steps back to back"},
+                       "l2": ("one input >> 126 MB L2, launches overlap 64 GiB apart"
+                              if len(slot_ptrs) == 1 else
+                              f"inputs larger than L2: {len(slot_ptrs)} copies of the input "
+                              f"({len(slot_ptrs) * nbytes >> 20} MiB), step i counts copy "
+                              f"i mod {len(slot_ptrs)}, steps back to back")},
             "cold_call": cold_call,
             "hbm_frac": round(value / world / peak, 4),
             "exact_reference": "C5: reference numba total of the 64 GiB array (golden.json)"

@@ -389,6 +389,77 @@ __device__ __forceinline__ uint32_t oh16pair(uint32_t c0, uint32_t c1) {
   return (shl32(1u, c0) & 0xFFFFu) | shl32(0x10000u, c1);
 }
 
+// u8 codes read one byte per lane straight from the shared-memory stage
+// (PP_CAT_LDS8, W = 16 / 32 / 64): LDS.U8 puts each code alone in a
+// register, so `shl` (which clamps amounts >= 32 to a zero result) makes
+// the one-hot word with no byte extraction and no range test, and no vote
+// for a small-code path -- the extraction moves from the ALU/FMA pipes to
+// the LSU.  Warp w owns bytes [w * 4096, (w + 1) * 4096) of the stage; its
+// j-th load reads 32 consecutive bytes (conflict-free).  Code slot j of a
+// lane sits at byte 32 * j + lane: any assignment works, the counts are a
+// histogram.  !FULL: slots at or past `lim` (bytes of this warp's slice
+// that hold codes) are no code.
+#ifndef PP_CAT_LDS8
+#define PP_CAT_LDS8 1
+#endif
+// 1 << n, 0 for n >= 32: one BMSK (a 1-bit mask at position n, clamped),
+// no register holding the constant 1 as `shl` needs
+__device__ __forceinline__ uint32_t bit_at(uint32_t n) {
+  uint32_t r;
+  asm("bmsk.clamp.b32 %0, %1, 1;" : "=r"(r) : "r"(n));
+  return r;
+}
+template <int W, bool FULL, class Ctr>
+__device__ __forceinline__ void eat_lds8(Ctr &c, const uint8_t *sb, int lim, const TC &t) {
+  auto code = [&](int j) -> uint32_t {
+    const int pos = 32 * j;  // + lane (sb is this lane's base)
+    if (FULL) return sb[pos];
+    return (pos < lim) ? (uint32_t)sb[pos] : 0xFFu;
+  };
+  if (W == 32) {  // one word per code: 4 groups of 32
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      uint4 u[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int j = 32 * g + 4 * q;
+        u[q] = make_uint4(bit_at(code(j)), bit_at(code(j + 1)), bit_at(code(j + 2)),
+                          bit_at(code(j + 3)));
+      }
+      c.csa(u, g);
+    }
+  } else if (W == 64) {  // (lo, hi) per code: 8 groups of 16
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      uint4 u[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t c0 = code(16 * g + 2 * q), c1 = code(16 * g + 2 * q + 1);
+        // c - 32 wraps for c < 32: any position >= 32 gives 0
+        u[q] = make_uint4(bit_at(c0), bit_at(c0 - 32u), bit_at(c1), bit_at(c1 - 32u));
+      }
+      c.csa(u, g);
+    }
+  } else {  // W == 16: two codes per word, 2 groups of 32 words
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      uint4 u[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        uint32_t wq[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = 64 * g + 8 * q + 2 * e;
+          wq[e] = (bit_at(code(j)) & 0xFFFFu) | (bit_at(code(j + 1) + 16u) & 0xFFFF0000u);
+        }
+        u[q] = make_uint4(wq[0], wq[1], wq[2], wq[3]);
+      }
+      c.csa(u, g);
+    }
+  }
+  c.end_chunk(t);
+}
+
 template <int W, bool FULL, int CB, class Ctr>
 __device__ __forceinline__ void eat_wide_codes(Ctr &c, const uint4 (&v)[8], uint32_t valid,
                                                const TC &t) {
@@ -551,6 +622,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       // start at once, and only the first ticket draw (the previous launch
       // on this stream may share the ticket counter) waits.
       bool waited = !a.input_ready;
+      if (a.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
       if (waited) asm volatile("griddepcontrol.wait;" ::: "memory");
       PP_TL(1);
       uint32_t stage = 0, phase = 0;
@@ -599,7 +671,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       PP_TL(3);
       // every load of this CTA is in flight: the next launch on the stream
       // (programmatic dependent launch) may start filling its own ring
-      asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+      if (!a.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     }
   } else {
     // ---------------- consumers
@@ -633,6 +705,28 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
 #endif
       if (first && threadIdx.x == 0) PP_TL(2);
       const uint4 *sv = stages + stage * Sh::kStageVecs;
+      if constexpr (PP_CAT_LDS8 && CB == 1 && (MODE == 16 || MODE == 32 || MODE == 64)) {
+        // u8 codes straight from the stage, one byte per lane (eat_lds8);
+        // the stage is released after the chunk is counted
+        constexpr int kSlice = (int)(Sh::kStageBytes / NCW);  // bytes per warp = 128 per lane
+        static_assert(kSlice == 32 * 128, "eat_lds8 expects 128 codes per lane");
+        const uint8_t *sb = reinterpret_cast<const uint8_t *>(sv) + warp * kSlice + lane;
+        const unsigned long long rem = a.body_bytes - ch * Sh::kStageBytes;
+        PP_CHK(stage < (uint32_t)Sh::kStages);
+        if (rem >= Sh::kStageBytes) {
+          eat_lds8<MODE, true>(c, sb, 0, t);
+        } else {
+          const long long lim = (long long)rem - (long long)warp * kSlice - (long long)lane;
+          eat_lds8<MODE, false>(c, sb, (int)(lim < 0 ? 0 : lim > kSlice ? kSlice : lim), t);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == Sh::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+        continue;
+      }
       uint4 v[8];
       uint32_t valid = 0xFFu;  // vectors present in this (possibly partial) chunk
       const unsigned long long off = ch * Sh::kStageBytes;
@@ -1032,10 +1126,27 @@ static cudaError_t launch_tma(Kern kernel, unsigned grid, unsigned block, size_t
   // base and the launch are one critical section: launches on a stream must
   // reach it in the order their bases were handed out.
   std::unique_lock<std::mutex> lk;
-  if (a.nchunks >= kDynMinChunks && units > 0) {
+  static const unsigned long long dyn_min = [] {  // A/B: PP_DYN_MIN_CHUNKS
+    const char *e = std::getenv("PP_DYN_MIN_CHUNKS");
+    return e ? std::strtoull(e, nullptr, 10) : kDynMinChunks;
+  }();
+  if (a.nchunks >= dyn_min && units > 0) {
     lk = sched_lock();
     a.sched = sched_slot(di, st, units, &a.sched_base);
   }
+  // Static-order launches (< 128 MiB) trigger the dependent launch at kernel
+  // start: this grid (<= one CTA per SM) is fully resident by then, the next
+  // grid's CTAs take the second shared-memory slot of each SM and (with
+  // INPUT_READY) stream their own input while this one drains -- back-to-
+  // back counts of distinct inputs overlap completely (C4 64 MiB 5650 ->
+  // 7125-7200 GB/s, C1 2 MiB 1222 -> 1387-1490); without INPUT_READY they
+  // only wait there (griddepcontrol.wait).  Ticketed launches trigger after
+  // each CTA's last load, as before: their successor cannot draw tickets
+  // before they complete, and the early trigger measured 0.9 % slower at
+  // 1 GiB (two interleaved streams).  scripts/gpu_trigger_ab.sh.  A/B:
+  // PP_LATE_TRIGGER=1 never triggers early.
+  static const int early = std::getenv("PP_LATE_TRIGGER") ? 0 : 1;
+  a.early_trigger = early && a.sched == nullptr;
 #if PP_CHECK_BOUNDS
   // per-launch {chunks consumed, CTAs finished} (stream-ordered scratch)
   if (cudaMallocAsync(reinterpret_cast<void **>(&a.chk_ctr), 16, st) != cudaSuccess ||

@@ -39,6 +39,9 @@ struct CountArgs {
   int input_ready;
   // static chunks per CTA before its first ticket (launch_tma: the ring depth)
   unsigned int lead;
+  // trigger the dependent launch at kernel start (default; PP_LATE_TRIGGER=1:
+  // after the CTA's last load)
+  int early_trigger;
   // checked builds (PP_CHECK_BOUNDS): the caller's byte range as the API
   // received it, and a per-launch {chunks consumed, CTAs finished} pair
   uintptr_t chk_lo, chk_hi;
