@@ -622,7 +622,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       // start at once, and only the first ticket draw (the previous launch
       // on this stream may share the ticket counter) waits.
       bool waited = !a.input_ready;
-      if (a.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+      bool triggered = a.early_trigger != 0;
+      if (triggered) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
       if (waited) asm volatile("griddepcontrol.wait;" ::: "memory");
       PP_TL(1);
       uint32_t stage = 0, phase = 0;
@@ -660,6 +661,13 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
           }
           ch = (unsigned long long)a.lead * gridDim.x +
                (unsigned long long)(atomicAdd(a.sched, 1u) - a.sched_base);
+          // tickets are drawn in order across the grid: once they reach the
+          // last trigger_tail chunks per CTA, let the next launch on the
+          // stream become resident and fill its ring (A/B: PP_TRIGGER_TAIL)
+          if (!triggered && ch + (unsigned long long)a.trigger_tail * gridDim.x >= nchunks) {
+            asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+            triggered = true;
+          }
         } else {
           ch += gridDim.x;
         }
@@ -671,7 +679,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       PP_TL(3);
       // every load of this CTA is in flight: the next launch on the stream
       // (programmatic dependent launch) may start filling its own ring
-      if (!a.early_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+      if (!triggered) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     }
   } else {
     // ---------------- consumers
@@ -1147,6 +1155,11 @@ static cudaError_t launch_tma(Kern kernel, unsigned grid, unsigned block, size_t
   // PP_LATE_TRIGGER=1 never triggers early.
   static const int early = std::getenv("PP_LATE_TRIGGER") ? 0 : 1;
   a.early_trigger = early && a.sched == nullptr;
+  static const unsigned tail = [] {
+    const char *e = std::getenv("PP_TRIGGER_TAIL");
+    return e ? (unsigned)std::atoi(e) : 0u;
+  }();
+  a.trigger_tail = tail;
 #if PP_CHECK_BOUNDS
   // per-launch {chunks consumed, CTAs finished} (stream-ordered scratch)
   if (cudaMallocAsync(reinterpret_cast<void **>(&a.chk_ctr), 16, st) != cudaSuccess ||

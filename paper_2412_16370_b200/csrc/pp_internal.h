@@ -42,6 +42,9 @@ struct CountArgs {
   // trigger the dependent launch at kernel start (default; PP_LATE_TRIGGER=1:
   // after the CTA's last load)
   int early_trigger;
+  // ticketed launches: trigger once tickets reach the last trigger_tail
+  // chunks per CTA (0: after the CTA's last load)
+  unsigned int trigger_tail;
   // checked builds (PP_CHECK_BOUNDS): the caller's byte range as the API
   // received it, and a per-launch {chunks consumed, CTAs finished} pair
   uintptr_t chk_lo, chk_hi;
