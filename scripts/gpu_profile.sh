@@ -3,7 +3,7 @@
 # command exited 0 without ncu.
 set -x
 python __graft_entry__.py > /dev/null 2>&1
-B="python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-check"
+B="python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-check --no-all-configs"
 $B > gpurun_out/prof_bench_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv $B > gpurun_out/ncu_launch_bench.log 2>&1; echo ncu_launch=$?
 P="python scripts/prof_kernels.py --reps 2"
