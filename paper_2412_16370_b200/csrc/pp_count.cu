@@ -159,36 +159,22 @@ __device__ __forceinline__ void fold_rows_to_counters(const unsigned long long (
 // fold with rot = 0:  W=8: four codes per word (byte k holds 1 << code_k),
 // W=16: two codes per word (half k), W=32: one code per word, W=64: one code
 // per (x|z = bits 0-31, y|w = bits 32-63) pair.  Codes >= W give no bit.
+// u8 codes at W >= 16 are read one byte per lane from shared memory
+// (eat_lds8); W = 8 and 2-/4-byte codes go through vector loads.
 
-// 4 u8 codes -> 4 one-hot bytes.  PRMT against the table {1,2,4,...,128}
-// turns nibble-packed codes into one-hot bytes in one instruction; bytes
-// whose code is >= 8 are cleared only when such a byte is present.
-__device__ __forceinline__ uint32_t onehot8x4(uint32_t x, bool any_big) {
-  const uint32_t xl = x & 0x07070707u;
-  const uint32_t tt = xl | (xl >> 4);
-  const uint32_t sel = (tt & 0xFFu) | ((tt >> 8) & 0xFF00u);
-  uint32_t oh = __byte_perm(0x08040201u, 0x80402010u, sel);
-  if (any_big) {
-    const uint32_t hi = x & 0xF8F8F8F8u;
-    const uint32_t nz = (((hi & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | hi) & 0x80808080u;
-    oh &= ~((nz >> 7) * 0xFFu);
-  }
-  return oh;
-}
-#ifndef PP_CAT_V2
-#define PP_CAT_V2 1
-#endif
-// v2 of the same: 2 ops for the nibble-packed selector (the LOP3 select
-// leaves junk only in the nibbles of codes >= 8, which the mask clears), and
-// a 5-op mask: z = (x | 0x80..) - 0x08.. has a byte's msb set iff that byte
-// is in [8, 0x80) (no borrow crosses a byte), x's msb covers [0x80, 0xFF];
-// PRMT's sign-replicate mode (selector nibble 8|i) widens msb -> 0xFF.
+// 4 u8 codes -> 4 one-hot bytes.  2 ops for the nibble-packed selector (the
+// LOP3 select leaves junk only in the nibbles of codes >= 8, which the mask
+// clears), one PRMT against the table {1,2,4,...,128}, and -- only when a
+// byte >= 8 is present -- a 5-op mask: z = (x | 0x80..) - 0x08.. has a
+// byte's msb set iff that byte is in [8, 0x80) (no borrow crosses a byte),
+// x's msb covers [0x80, 0xFF]; PRMT's sign-replicate mode (selector nibble
+// 8|i) widens msb -> 0xFF.
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
   uint32_t d;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
   return d;
 }
-__device__ __forceinline__ uint32_t onehot8x4_v2(uint32_t x, bool any_big) {
+__device__ __forceinline__ uint32_t onehot8x4(uint32_t x, bool any_big) {
   uint32_t tt;  // (x & 0x07070707) | ((x >> 4) & ~0x07070707): one LOP3
   asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(tt) : "r"(x), "r"(x >> 4), "r"(0x07070707u));
   const uint32_t sel = prmt(tt, 0u, 0x0020u);  // nibbles: code0..code3 (low 16 bits)
@@ -204,125 +190,30 @@ __device__ __forceinline__ void onehot64(uint32_t c, uint32_t &lo, uint32_t &hi)
   asm("{\n\t.reg .b64 t;\n\tmov.b64 t, 1;\n\tshl.b64 t, t, %2;\n\tmov.b64 {%0, %1}, t;\n\t}"
       : "=r"(lo), "=r"(hi) : "r"(c));
 }
-
-// byte k of x, zero-extended: one PRMT
-__device__ __forceinline__ uint32_t byte_of(uint32_t x, int k) {
-  return __byte_perm(x, 0u, 0x4440u | (uint32_t)k);
-}
-// 2 u8 codes (bytes k, k+1 of x) -> one word with 16-bit one-hot halves
-__device__ __forceinline__ uint32_t onehot16x2(uint32_t x, int k) {
-  const uint32_t a = byte_of(x, k), b = byte_of(x, k + 1);
-  uint32_t lo, hi;
-  asm("shl.b32 %0, 1, %1;" : "=r"(lo) : "r"(a));        // >= 32 -> 0 (clamped)
-  asm("shl.b32 %0, 65536, %1;" : "=r"(hi) : "r"(b));    // >= 16 -> 0
-  return (lo & 0xFFFFu) | hi;
-}
 __device__ __forceinline__ uint32_t onehot32(uint32_t c) {
   uint32_t r;
   asm("shl.b32 %0, 1, %1;" : "=r"(r) : "r"(c));  // c >= 32 -> 0
   return r;
 }
 
-// Expand and count 8 vectors (128 u8 codes) of one thread; vectors with
-// valid bit i clear are absent (partial last chunk) and contribute nothing.
-// FULL: every vector present (all but the last chunk) -- no per-word selects.
-template <int W, bool FULL, class Ctr>
-__device__ __forceinline__ void eat_codes(Ctr &c, const uint4 (&v)[8], uint32_t valid,
-                                          const TC &t) {
-  const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
-  if (W == 8) {
-    uint4 u[8];
+// Expand and count 8 vectors (128 u8 codes, W = 8) of one thread; vectors
+// with valid bit i clear are absent (partial last chunk) and contribute
+// nothing.  FULL: every vector present (all but the last chunk).
+template <bool FULL, class Ctr>
+__device__ __forceinline__ void eat_codes8(Ctr &c, const uint4 (&v)[8], uint32_t valid,
+                                           const TC &t) {
+  uint4 u[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const bool big = ((v[i].x | v[i].y | v[i].z | v[i].w) & 0xF8F8F8F8u) != 0;
-#if PP_CAT_V2
-      u[i] = make_uint4(onehot8x4_v2(v[i].x, big), onehot8x4_v2(v[i].y, big),
-                        onehot8x4_v2(v[i].z, big), onehot8x4_v2(v[i].w, big));
-#else
-      u[i] = make_uint4(onehot8x4(v[i].x, big), onehot8x4(v[i].y, big),
-                        onehot8x4(v[i].z, big), onehot8x4(v[i].w, big));
-#endif
-      if (!FULL && !((valid >> i) & 1u)) u[i] = z4;
-    }
-    c.csa(u, 0);
-  } else if (W == 16) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      uint4 u[8];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint4 x = v[4 * h + i];
-        const bool ok = FULL || ((valid >> (4 * h + i)) & 1u);
-        u[2 * i] = ok ? make_uint4(onehot16x2(x.x, 0), onehot16x2(x.x, 2), onehot16x2(x.y, 0),
-                                   onehot16x2(x.y, 2))
-                      : z4;
-        u[2 * i + 1] = ok ? make_uint4(onehot16x2(x.z, 0), onehot16x2(x.z, 2),
-                                       onehot16x2(x.w, 0), onehot16x2(x.w, 2))
-                          : z4;
-      }
-      c.csa(u, h);
-    }
-  } else if (W == 32) {
-#pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      uint4 u[8];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const uint4 x = v[2 * h + i];
-        const bool ok = FULL || ((valid >> (2 * h + i)) & 1u);
-        const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t wd = w4[q];
-          u[4 * i + q] = ok ? make_uint4(onehot32(wd & 0xFFu), onehot32(byte_of(wd, 1)),
-                                         onehot32(byte_of(wd, 2)), onehot32(wd >> 24))
-                            : z4;
-        }
-      }
-      c.csa(u, h);
-    }
-  } else {  // W == 64: code c -> (x|z, y|w) = (1 << c, 1 << (c - 32))
-#pragma unroll
-    for (int h = 0; h < 8; ++h) {
-      const uint4 x = v[h];
-      const bool ok = FULL || ((valid >> h) & 1u);
-      const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
-      uint4 u[8];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const uint32_t c0 = byte_of(w4[q], 2 * k), c1 = byte_of(w4[q], 2 * k + 1);
-#if PP_CAT_V2
-          uint32_t l0, h0, l1, h1;
-          onehot64(c0, l0, h0);
-          onehot64(c1, l1, h1);
-          u[2 * q + k] = ok ? make_uint4(l0, h0, l1, h1) : z4;
-#else
-          u[2 * q + k] = ok ? make_uint4(onehot32(c0), onehot32(c0 - 32u), onehot32(c1),
-                                         onehot32(c1 - 32u))
-                            : z4;
-#endif
-        }
-      }
-      c.csa(u, h);
-    }
+  for (int i = 0; i < 8; ++i) {
+    const bool big = ((v[i].x | v[i].y | v[i].z | v[i].w) & 0xF8F8F8F8u) != 0;
+    u[i] = make_uint4(onehot8x4(v[i].x, big), onehot8x4(v[i].y, big), onehot8x4(v[i].z, big),
+                      onehot8x4(v[i].w, big));
+    if (!FULL && !((valid >> i) & 1u)) u[i] = make_uint4(0u, 0u, 0u, 0u);
   }
+  c.csa(u, 0);
   c.end_chunk(t);
 }
 
-// Fast path for W = 32 when every code of the warp's 8 vectors is < 32 (the
-// caller votes): no range handling, so a code needs no clean byte -- SHF.L.W
-// takes its shift amount mod 32 -- and bytes 1-3 are brought down with
-// IMAD.HI (mul.hi by 2^(32-8k); ptxas keeps it on the FMA pipe) instead of
-// PRMT / SHF on the ALU pipe.  Per 4 codes: 4 SHF on the ALU pipe + 3 IMAD.HI,
-// vs 8 ALU ops in eat_codes.  Measured: ALU pipe 95 -> 79 %, but the kernel
-// is then latency-/dispatch-limited (16 consumer warps): 3889 -> 3982 GB/s
-// (profiles/r1_categories_ablation.md).  The same trick at W = 16 (two codes
-// per word) saves no instructions and its vote costs 3.5 %: not used there.
-#ifndef PP_CAT_SMALL
-#define PP_CAT_SMALL 1
-#endif
 // eat8 groups per chunk of one thread (8 vectors of CB-byte codes): the
 // one-hot words of 128 / CB codes, W / 32 words per code (W = 8: four codes
 // per word, 16: two), 32 words per group
@@ -333,41 +224,6 @@ constexpr int groups_per_chunk() {
 // the fused producer's counter: one tree at W <= 32, two at W = 64
 template <int W, int CB>
 using CatCtr = CatCounter<W == 64 ? 2 : 1, (W == 64 ? 1 : 2) * groups_per_chunk<W, CB>()>;
-#ifndef PP_CAT_SMALL_MULHI  // 0: plain shifts (ALU) for bytes 1-3 (A/B)
-#define PP_CAT_SMALL_MULHI 1
-#endif
-__device__ __forceinline__ uint32_t hi_bytes(uint32_t x, int k) {  // x >> 8k, k = 1..3
-#if PP_CAT_SMALL_MULHI
-  uint32_t r;
-  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(1u << (32 - 8 * k)));
-  return r;
-#else
-  return x >> (8 * k);
-#endif
-}
-__device__ __forceinline__ uint32_t oh_wrap(uint32_t n) {  // 1 << (n mod 32)
-  return __funnelshift_l(0u, 1u, n);
-}
-template <class Ctr>
-__device__ __forceinline__ void eat_small_codes32(Ctr &c, const uint4 (&v)[8], const TC &t) {
-#pragma unroll
-  for (int h = 0; h < 4; ++h) {
-    uint4 u[8];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const uint4 x = v[2 * h + i];
-      const uint32_t w4[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t wd = w4[q];
-        u[4 * i + q] = make_uint4(oh_wrap(wd), oh_wrap(hi_bytes(wd, 1)), oh_wrap(hi_bytes(wd, 2)),
-                                  oh_wrap(hi_bytes(wd, 3)));
-      }
-    }
-    c.csa(u, h);
-  }
-  c.end_chunk(t);
-}
 
 // 2- / 4-byte codes (CB = code bytes): the same packed one-hot words, built
 // from wider lanes.  shl clamps any shift amount >= the register width to a
@@ -390,7 +246,7 @@ __device__ __forceinline__ uint32_t oh16pair(uint32_t c0, uint32_t c1) {
 }
 
 // u8 codes read one byte per lane straight from the shared-memory stage
-// (PP_CAT_LDS8, W = 16 / 32 / 64): LDS.U8 puts each code alone in a
+// (W = 16 / 32 / 64): LDS.U8 puts each code alone in a
 // register, so `shl` (which clamps amounts >= 32 to a zero result) makes
 // the one-hot word with no byte extraction and no range test, and no vote
 // for a small-code path -- the extraction moves from the ALU/FMA pipes to
@@ -399,9 +255,6 @@ __device__ __forceinline__ uint32_t oh16pair(uint32_t c0, uint32_t c1) {
 // lane sits at byte 32 * j + lane: any assignment works, the counts are a
 // histogram.  !FULL: slots at or past `lim` (bytes of this warp's slice
 // that hold codes) are no code.
-#ifndef PP_CAT_LDS8
-#define PP_CAT_LDS8 1
-#endif
 // 1 << n, 0 for n >= 32: one BMSK (a 1-bit mask at position n, clamped),
 // no register holding the constant 1 as `shl` needs
 __device__ __forceinline__ uint32_t bit_at(uint32_t n) {
@@ -713,7 +566,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
 #endif
       if (first && threadIdx.x == 0) PP_TL(2);
       const uint4 *sv = stages + stage * Sh::kStageVecs;
-      if constexpr (PP_CAT_LDS8 && CB == 1 && (MODE == 16 || MODE == 32 || MODE == 64)) {
+      if constexpr (CB == 1 && (MODE == 16 || MODE == 32 || MODE == 64)) {
         // u8 codes straight from the stage, one byte per lane (eat_lds8);
         // the stage is released after the chunk is counted
         constexpr int kSlice = (int)(Sh::kStageBytes / NCW);  // bytes per warp = 128 per lane
@@ -755,40 +608,22 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
-      // W = 32 u8 codes: vote (whole warp, converged here) for the fast
-      // path -- full chunk and every code < 32
-      bool small = false;
-      if (PP_CAT_SMALL && MODE == 32 && CB == 1) {
-        uint32_t o = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o |= v[i].x | v[i].y | v[i].z | v[i].w;
-        small = __all_sync(FULL, valid == 0xFFu && (o & 0xE0E0E0E0u) == 0u);
-      }
       if constexpr (MODE == 1) {
         c.eat8(v, t);
-      } else if constexpr (MODE >= 8 && CB == 1) {
-        bool done = false;
-        if constexpr (MODE == 32) {
-          if (small) {
-            eat_small_codes32(c, v, t);
-            done = true;
-          }
-        }
-        if (!done) {
-          if (valid == 0xFFu)
-            eat_codes<MODE, true>(c, v, valid, t);
-          else
-            eat_codes<MODE, false>(c, v, valid, t);
-        }
-      } else if constexpr (MODE >= 8) {
+      } else if constexpr (MODE == 8 && CB == 1) {
+        if (valid == 0xFFu)
+          eat_codes8<true>(c, v, valid, t);
+        else
+          eat_codes8<false>(c, v, valid, t);
+      } else if constexpr (MODE >= 8 && CB > 1) {
         if (valid == 0xFFu)
           eat_wide_codes<MODE, true, CB>(c, v, valid, t);
         else
           eat_wide_codes<MODE, false, CB>(c, v, valid, t);
-      } else {
+      } else if constexpr (MODE == 0) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) xs ^= v[i].x ^ v[i].y ^ v[i].z ^ v[i].w;
-      }
+      }  // (u8 codes at W >= 16 took the eat_lds8 path above)
       if (++stage == Sh::kStages) {
         stage = 0;
         phase ^= 1;
@@ -1155,9 +990,15 @@ static cudaError_t launch_tma(Kern kernel, unsigned grid, unsigned block, size_t
   // PP_LATE_TRIGGER=1 never triggers early.
   static const int early = std::getenv("PP_LATE_TRIGGER") ? 0 : 1;
   a.early_trigger = early && a.sched == nullptr;
+  // ticketed launches trigger their successor once the tickets reach the
+  // last 4 chunks per CTA: it becomes resident and fills its ring (static
+  // lead chunks, INPUT_READY) during this launch's last ~3 us instead of
+  // after its last load (1 GiB: 7450 -> 7528 GB/s; tail 2 / 4 / 8 / 16 =
+  // 7508-7519 / 7525-7530 / 7511-7517 / 7290, scripts/gpu_tail_ab.sh).
+  // A/B: PP_TRIGGER_TAIL=n (0 = after the CTA's last load).
   static const unsigned tail = [] {
     const char *e = std::getenv("PP_TRIGGER_TAIL");
-    return e ? (unsigned)std::atoi(e) : 0u;
+    return e ? (unsigned)std::atoi(e) : 4u;
   }();
   a.trigger_tail = tail;
 #if PP_CHECK_BOUNDS
