@@ -303,7 +303,9 @@ __device__ __forceinline__ void eat_lds8(Ctr &c, const uint8_t *sb, int lim, con
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int j = 64 * g + 8 * q + 2 * e;
-          wq[e] = (bit_at(code(j)) & 0xFFFFu) | (bit_at(code(j + 1) + 16u) & 0xFFFF0000u);
+          // low halves of the two one-hot words (codes 16..31 fall in the
+          // dropped high halves): one PRMT
+          wq[e] = prmt(bit_at(code(j)), bit_at(code(j + 1)), 0x5410u);
         }
         u[q] = make_uint4(wq[0], wq[1], wq[2], wq[3]);
       }
