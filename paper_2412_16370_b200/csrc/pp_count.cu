@@ -288,8 +288,11 @@ __device__ __forceinline__ void eat_lds8(Ctr &c, const uint8_t *sb, int lim, con
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const uint32_t c0 = code(16 * g + 2 * q), c1 = code(16 * g + 2 * q + 1);
-        // c - 32 wraps for c < 32: any position >= 32 gives 0
-        u[q] = make_uint4(bit_at(c0), bit_at(c0 - 32u), bit_at(c1), bit_at(c1 - 32u));
+        // 1 << c as a 64-bit shift: two SHF (the clamp makes c >= 64 vanish)
+        uint32_t l0, h0, l1, h1;
+        onehot64(c0, l0, h0);
+        onehot64(c1, l1, h1);
+        u[q] = make_uint4(l0, h0, l1, h1);
       }
       c.csa(u, g);
     }
