@@ -485,9 +485,10 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       if (waited) asm volatile("griddepcontrol.wait;" ::: "memory");
       PP_TL(1);
       uint32_t stage = 0, phase = 0;
-      // chunk sequence: chunk blockIdx.x first, then either dynamic (ticket
-      // t of a shared counter = chunk gridDim.x + t, so every CTA finishes
-      // within about one chunk of the others) or the static grid stride
+      // chunk sequence: the static grid stride (blockIdx.x + j * gridDim.x),
+      // for ticketed launches only the first a.lead chunks, then ticket t of
+      // the stream's counter = chunk a.lead * gridDim.x + t, so every CTA
+      // finishes within about one chunk of the others
       unsigned long long ch = blockIdx.x;
       uint32_t issued = 0;  // chunks this CTA has issued
       for (;;) {
