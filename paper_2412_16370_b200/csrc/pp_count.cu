@@ -225,6 +225,33 @@ constexpr int groups_per_chunk() {
 template <int W, int CB>
 using CatCtr = CatCounter<W == 64 ? 2 : 1, (W == 64 ? 1 : 2) * groups_per_chunk<W, CB>()>;
 
+// 2-byte codes at W = 64 (the one wide-code case that is ALU-bound), the
+// same way: LDS.U16 puts each code alone in a register, `1 << c` is one
+// 64-bit shift (amounts >= 64 give 0, so negative / large codes vanish).
+// Warp w owns 4 KiB of the stage = 64 codes per lane; code slot j of a lane
+// sits at code index 32 * j + lane.  !FULL: slots at or past `lim` (codes of
+// this warp's slice that exist) are no code.
+template <bool FULL, class Ctr>
+__device__ __forceinline__ void eat_lds16_w64(Ctr &c, const uint16_t *sb, int lim, const TC &t) {
+  auto code = [&](int j) -> uint32_t {
+    if (FULL) return sb[32 * j];
+    return (32 * j < lim) ? (uint32_t)sb[32 * j] : 0xFFFFu;
+  };
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {  // 4 groups of 16 codes (32 words)
+    uint4 u[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      uint32_t l0, h0, l1, h1;
+      onehot64(code(16 * g + 2 * q), l0, h0);
+      onehot64(code(16 * g + 2 * q + 1), l1, h1);
+      u[q] = make_uint4(l0, h0, l1, h1);
+    }
+    c.csa(u, g);
+  }
+  c.end_chunk(t);
+}
+
 // 2- / 4-byte codes (CB = code bytes): the same packed one-hot words, built
 // from wider lanes.  shl clamps any shift amount >= the register width to a
 // zero result, so codes >= W need no test however large they are; the
@@ -572,6 +599,28 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
 #endif
       if (first && threadIdx.x == 0) PP_TL(2);
       const uint4 *sv = stages + stage * Sh::kStageVecs;
+      if constexpr (CB == 2 && MODE == 64) {
+        // 2-byte codes at W = 64: one code per lane from the stage
+        constexpr int kSlice = (int)(Sh::kStageBytes / NCW);  // bytes per warp
+        static_assert(kSlice == 2 * 32 * 64, "eat_lds16_w64 expects 64 codes per lane");
+        const uint16_t *sb =
+            reinterpret_cast<const uint16_t *>(reinterpret_cast<const uint8_t *>(sv) +
+                                               warp * kSlice) + lane;
+        const unsigned long long rem = a.body_bytes - ch * Sh::kStageBytes;
+        if (rem >= Sh::kStageBytes) {
+          eat_lds16_w64<true>(c, sb, 0, t);
+        } else {
+          const long long lim = ((long long)rem - (long long)warp * kSlice) / 2 - (long long)lane;
+          eat_lds16_w64<false>(c, sb, (int)(lim < 0 ? 0 : lim > kSlice / 2 ? kSlice / 2 : lim), t);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == Sh::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+        continue;
+      }
       if constexpr (CB == 1 && (MODE == 16 || MODE == 32 || MODE == 64)) {
         // u8 codes straight from the stage, one byte per lane (eat_lds8);
         // the stage is released after the chunk is counted
@@ -621,7 +670,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
           eat_codes8<true>(c, v, valid, t);
         else
           eat_codes8<false>(c, v, valid, t);
-      } else if constexpr (MODE >= 8 && CB > 1) {
+      } else if constexpr (MODE >= 8 && CB > 1 && !(CB == 2 && MODE == 64)) {
         if (valid == 0xFFu)
           eat_wide_codes<MODE, true, CB>(c, v, valid, t);
         else
