@@ -382,6 +382,31 @@ def require_devices(n, local=None):
                          f"devices: {devs}")
 
 
+def bind_to_gpu_numa_node(local):
+    """Pin this rank's host threads to the CPUs NVML names as closest to its
+    GPU (N > 1 only): the rank's pinned host buffers are then first-touched
+    on the GPU's own NUMA node, so N ranks' host->device copies do not all
+    cross the socket interconnect.  Returns the CPU count, or None."""
+    try:
+        import pynvml
+        import torch
+        uuid = str(torch.cuda.get_device_properties(local).uuid)
+        pynvml.nvmlInit()
+        try:
+            h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        finally:
+            pynvml.nvmlShutdown()
+        cpus = {64 * i + b for i, wd in enumerate(words) for b in range(64) if (wd >> b) & 1}
+        cpus &= set(range(os.cpu_count() or 1))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return len(cpus)
+    except Exception as exc:  # noqa: BLE001 - an optimisation, never a failure
+        print(f"bench: no NUMA binding ({exc})", file=sys.stderr)
+    return None
+
+
 def run_strong_c5(args, lib, world, rank, dev, st, use_dist, peers):
     """C5 (BASELINE.json configs[4]): the 64 GiB w=16 array with p ~ U[0,1]
     per 1 MiB block, split over the N ranks in contiguous 64-byte-cut shards
@@ -483,6 +508,7 @@ def main_gpu(args):
         require_devices(world, local)
     local = int(os.environ.get("PP_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
+    numa_cpus = bind_to_gpu_numa_node(local) if world > 1 else None
     dev = torch.device("cuda", local)
     # under torchrun (even with one rank) the NCCL path runs: every step ends
     # with the allreduce of the counters; plain `python bench.py` is N=1 local
@@ -1049,6 +1075,8 @@ def main_gpu(args):
             "launch": ("pp_count_ex(..., PP_COUNT_INPUT_READY): inputs written once before "
                        "the first count, so a step's loads may overlap the previous step's tail"
                        if count_flags and seg_out is None else "plain launches"),
+            "host_binding": (f"each rank's host threads pinned to its GPU's NUMA-local CPUs "
+                             f"(rank 0: {numa_cpus})" if numa_cpus else None),
             "exchange": ("none (rows stay on their rank)" if seg_out is not None else
                          "fused: the counting kernel adds into every rank's IPC-mapped "
                          "counters (pp_count_multi)" if fused else
