@@ -69,8 +69,8 @@ def _worker(rank, world, port, total, lead, width, seed):
             part = full[cut[rank]:cut[rank + 1]]
         else:
             part = full[lo:hi]
-        for _ in range(3):
-            peers.count(part.data_ptr(), part.numel(), width)
+        for i in range(3):  # the buffer is written before any count: input_ready holds
+            peers.count(part.data_ptr(), part.numel(), width, input_ready=bool(i % 2))
         peers.sync()
         assert [int(x) for x in peers.local[:width].cpu()] == [3 * v for v in want]
         # an empty shard is fine (its CTAs add zeros)
