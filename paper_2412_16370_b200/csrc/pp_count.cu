@@ -70,6 +70,39 @@ struct TmaShape {
 #endif
 using CatShape = TmaShape<PP_CAT_NCW>;
 
+// One-hot words from a shared-memory table (u8 codes at W = 64): for
+// PP_CAT_TAB64 of every 16 codes of a chunk (a static share; 0 = off) the
+// (lo, hi) one-hot pair is LOADED from a per-lane table -- entry c of lane l
+// at c * 256 + l * 8 bytes: every lane has its own banks, so the loads are
+// conflict-free whatever the codes; entries c >= 64 are zero, so large codes
+// and absent slots (0xFF) vanish -- at an address made by one IMAD, instead
+// of being computed by two ALU shifts.  The counter's LOP3s keep more of the
+// ALU pipe and the LSU / FMA pipes, mostly idle otherwise, carry part of the
+// one-hot step; the share balances the ALU pipe (3.1 - 1.0 f clk per 32
+// codes per SM) against the LSU (1 + 2 f): 11/16 measured best (0 / 6 / 8 /
+// 10 / 11 / 12 / 14 / 16 of 16 = 2806 / 3113 / 3196 / 3280 / 3291 / 3204 /
+// 2992 / 2803 G codes/s, scripts/gpu_cat_tab.sh).  The 64 KiB table takes
+// the third stage's shared memory: this kernel runs a 2-stage ring (no loss
+// at its 3.3 TB/s).  At W = 32 the same scheme (LDS.32 table, best share
+// 8/32) measured +1.3 % only, less than its 2-stage ring costs at 5.3 TB/s;
+// not kept.
+#ifndef PP_CAT_TAB64
+#define PP_CAT_TAB64 11
+#endif
+#ifndef PP_CAT_TAB_STAGES
+#define PP_CAT_TAB_STAGES 2
+#endif
+template <int MODE, int NCW, int CB>
+struct KShape {
+  using Sh = TmaShape<NCW>;
+  static constexpr int kTabEntry = (CB == 1 && MODE == 64 && PP_CAT_TAB64 > 0) ? 8 : 0;
+  static constexpr int kTabBytes = 256 * 32 * kTabEntry;
+  static constexpr int kStages = kTabBytes ? PP_CAT_TAB_STAGES : Sh::kStages;
+  static constexpr size_t kBarOff = kStages * Sh::kStageBytes;
+  static constexpr size_t kTabOff = (kBarOff + 2 * kStages * 8 + 15) & ~(size_t)15;
+  static constexpr size_t kSmem = kTabOff + kTabBytes;
+};
+
 constexpr int kLdgWarps = 8;
 constexpr int kLdgThreads = kLdgWarps * 32;
 constexpr int kLdgChunkVecs = kLdgThreads * 8;
@@ -289,8 +322,22 @@ __device__ __forceinline__ uint32_t bit_at(uint32_t n) {
   asm("bmsk.clamp.b32 %0, %1, 1;" : "=r"(r) : "r"(n));
   return r;
 }
+// table entry of code c for this lane (tab = shared address of the lane's
+// column, mul = bytes per table row, a kernel argument so that the address
+// is one IMAD on the FMA pipe and not shifts/adds on the ALU pipe)
+__device__ __forceinline__ void tab_load64(uint32_t c, uint32_t mul, uint32_t tab, uint32_t &lo,
+                                           uint32_t &hi) {
+  uint32_t addr;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(c), "r"(mul), "r"(tab));
+  asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(addr));
+}
+// slot k of every n takes the table path when this is true: `share` of n, spread evenly
+__host__ __device__ constexpr bool tab_slot(int k, int n, int share) {
+  return ((k + 1) * share / n) != (k * share / n);
+}
 template <int W, bool FULL, class Ctr>
-__device__ __forceinline__ void eat_lds8(Ctr &c, const uint8_t *sb, int lim, const TC &t) {
+__device__ __forceinline__ void eat_lds8(Ctr &c, const uint8_t *sb, int lim, const TC &t,
+                                         uint32_t tab, uint32_t mul) {
   auto code = [&](int j) -> uint32_t {
     const int pos = 32 * j;  // + lane (sb is this lane's base)
     if (FULL) return sb[pos];
@@ -314,12 +361,16 @@ __device__ __forceinline__ void eat_lds8(Ctr &c, const uint8_t *sb, int lim, con
       uint4 u[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const uint32_t c0 = code(16 * g + 2 * q), c1 = code(16 * g + 2 * q + 1);
-        // 1 << c as a 64-bit shift: two SHF (the clamp makes c >= 64 vanish)
-        uint32_t l0, h0, l1, h1;
-        onehot64(c0, l0, h0);
-        onehot64(c1, l1, h1);
-        u[q] = make_uint4(l0, h0, l1, h1);
+        uint32_t l[2], h[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const uint32_t ce = code(16 * g + 2 * q + e);
+          if (tab_slot(2 * q + e, 16, PP_CAT_TAB64))
+            tab_load64(ce, mul, tab, l[e], h[e]);
+          else  // 1 << c as a 64-bit shift: two SHF (the clamp makes c >= 64 vanish)
+            onehot64(ce, l[e], h[e]);
+        }
+        u[q] = make_uint4(l[0], h[0], l[1], h[1]);
       }
       c.csa(u, g);
     }
@@ -475,24 +526,32 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     pp_tma_kernel(CountArgs a, unsigned long long *sink) {
   constexpr bool kCount = MODE != 0;
   using Sh = TmaShape<NCW>;
+  using KS = KShape<MODE, NCW, CB>;
   extern __shared__ __align__(128) uint8_t smem[];
   uint4 *stages = reinterpret_cast<uint4 *>(smem);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + Sh::kStages * Sh::kStageBytes);
-  uint64_t *empty = full + Sh::kStages;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + KS::kBarOff);
+  uint64_t *empty = full + KS::kStages;
   __shared__ unsigned long long frame[PP_EPI_SLOTS ? 1 : 64];
   __shared__ unsigned long long wframe[PP_EPI_SLOTS ? NCW : 1][64];  // per-warp frame rows
-  __shared__ unsigned long long chunk_id[Sh::kStages];  // written before the stage's arrival
+  __shared__ unsigned long long chunk_id[KS::kStages];  // written before the stage's arrival
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     PP_TL(0);
-    for (int s = 0; s < Sh::kStages; ++s) {
+    for (int s = 0; s < KS::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NCW);
     }
     fence_mbar_init();
   }
   if (!PP_EPI_SLOTS && threadIdx.x < 64) frame[threadIdx.x] = 0;
+  if constexpr (KS::kTabBytes != 0) {  // per-lane one-hot tables (see KShape)
+    for (uint32_t i = threadIdx.x; i < 256u * 32u; i += (NCW + 1) * 32) {
+      uint32_t lo, hi;
+      onehot64(i >> 5, lo, hi);  // entry i / 32, lane i % 32
+      reinterpret_cast<uint2 *>(smem + KS::kTabOff)[i] = make_uint2(lo, hi);
+    }
+  }
   __syncthreads();
 
   const unsigned long long nchunks = a.nchunks;
@@ -529,7 +588,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         const unsigned long long off = ch * Sh::kStageBytes;
         const unsigned long long rem = a.body_bytes - off;
         const uint32_t bytes = (uint32_t)(rem < Sh::kStageBytes ? rem : Sh::kStageBytes);
-        if (PP_CHK(stage < (uint32_t)Sh::kStages) &&
+        if (PP_CHK(stage < (uint32_t)KS::kStages) &&
             PP_CHK_RANGE(a.body + off, bytes, a.chk_lo, a.chk_hi)) {
           mbar_arrive_expect_tx(&full[stage], bytes);
           bulk_g2s(stages + stage * Sh::kStageVecs, a.body + off, bytes, &full[stage], pol);
@@ -557,7 +616,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         } else {
           ch += gridDim.x;
         }
-        if (++stage == Sh::kStages) {
+        if (++stage == KS::kStages) {
           stage = 0;
           phase ^= 1;
         }
@@ -615,7 +674,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
-        if (++stage == Sh::kStages) {
+        if (++stage == KS::kStages) {
           stage = 0;
           phase ^= 1;
         }
@@ -628,16 +687,19 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         static_assert(kSlice == 32 * 128, "eat_lds8 expects 128 codes per lane");
         const uint8_t *sb = reinterpret_cast<const uint8_t *>(sv) + warp * kSlice + lane;
         const unsigned long long rem = a.body_bytes - ch * Sh::kStageBytes;
-        PP_CHK(stage < (uint32_t)Sh::kStages);
+        PP_CHK(stage < (uint32_t)KS::kStages);
+        const uint32_t tab =
+            (uint32_t)__cvta_generic_to_shared(smem + KS::kTabOff) + lane * KS::kTabEntry;
         if (rem >= Sh::kStageBytes) {
-          eat_lds8<MODE, true>(c, sb, 0, t);
+          eat_lds8<MODE, true>(c, sb, 0, t, tab, a.tab_mul);
         } else {
           const long long lim = (long long)rem - (long long)warp * kSlice - (long long)lane;
-          eat_lds8<MODE, false>(c, sb, (int)(lim < 0 ? 0 : lim > kSlice ? kSlice : lim), t);
+          eat_lds8<MODE, false>(c, sb, (int)(lim < 0 ? 0 : lim > kSlice ? kSlice : lim), t, tab,
+                                a.tab_mul);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
-        if (++stage == Sh::kStages) {
+        if (++stage == KS::kStages) {
           stage = 0;
           phase ^= 1;
         }
@@ -648,7 +710,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       const unsigned long long off = ch * Sh::kStageBytes;
       const unsigned long long rem = a.body_bytes - off;
       if (rem >= Sh::kStageBytes) {
-        PP_CHK(stage < (uint32_t)Sh::kStages && tid + 7 * (NCW * 32) < (uint32_t)Sh::kStageVecs);
+        PP_CHK(stage < (uint32_t)KS::kStages && tid + 7 * (NCW * 32) < (uint32_t)Sh::kStageVecs);
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = sv[tid + i * (NCW * 32)];
       } else {
@@ -679,7 +741,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
 #pragma unroll
         for (int i = 0; i < 8; ++i) xs ^= v[i].x ^ v[i].y ^ v[i].z ^ v[i].w;
       }  // (u8 codes at W >= 16 took the eat_lds8 path above)
-      if (++stage == Sh::kStages) {
+      if (++stage == KS::kStages) {
         stage = 0;
         phase ^= 1;
       }
@@ -802,15 +864,15 @@ static cudaError_t compute_device_info(int dev, DevInfo *out) {
   if ((e = cudaFuncSetAttribute(pp_tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kTmaSmemBytes)))
     return e;
-  for (auto k : {pp_tma_kernel<8, PP_CAT_NCW>, pp_tma_kernel<16, PP_CAT_NCW>,
-                 pp_tma_kernel<32, PP_CAT_NCW>, pp_tma_kernel<64, PP_CAT_NCW>,
-                 pp_tma_kernel<8, PP_CAT_NCW, 2>, pp_tma_kernel<16, PP_CAT_NCW, 2>,
-                 pp_tma_kernel<32, PP_CAT_NCW, 2>, pp_tma_kernel<64, PP_CAT_NCW, 2>,
-                 pp_tma_kernel<8, PP_CAT_NCW, 4>, pp_tma_kernel<16, PP_CAT_NCW, 4>,
-                 pp_tma_kernel<32, PP_CAT_NCW, 4>, pp_tma_kernel<64, PP_CAT_NCW, 4>})
-    if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)CatShape::kSmem)))
-      return e;
+#define PP_CAT_ATTR(W, CB)                                                              \
+  if ((e = cudaFuncSetAttribute(pp_tma_kernel<W, PP_CAT_NCW, CB>,                        \
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,             \
+                                (int)KShape<W, PP_CAT_NCW, CB>::kSmem)))                 \
+    return e;
+  PP_CAT_ATTR(8, 1) PP_CAT_ATTR(16, 1) PP_CAT_ATTR(32, 1) PP_CAT_ATTR(64, 1)
+  PP_CAT_ATTR(8, 2) PP_CAT_ATTR(16, 2) PP_CAT_ATTR(32, 2) PP_CAT_ATTR(64, 2)
+  PP_CAT_ATTR(8, 4) PP_CAT_ATTR(16, 4) PP_CAT_ATTR(32, 4) PP_CAT_ATTR(64, 4)
+#undef PP_CAT_ATTR
   if ((e = segmented_setup(&d))) return e;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.ldg_blocks_per_sm,
                                                          pp_count_ldg_kernel, kLdgThreads, 0)))
@@ -1105,22 +1167,23 @@ cudaError_t launch_count(const CountArgs &a, LoadPath path, const DevInfo &di,
   return cudaGetLastError();
 }
 
+template <int W, int CB>
+static cudaError_t launch_codes_w(const CountArgs &a0, unsigned g, const DevInfo &di,
+                                  cudaStream_t st) {
+  using KS = KShape<W, PP_CAT_NCW, CB>;
+  CountArgs a = a0;
+  a.tab_mul = 32u * KS::kTabEntry;  // bytes per table row (0: no table)
+  return launch_tma(pp_tma_kernel<W, PP_CAT_NCW, CB>, g, CatShape::kThreads, KS::kSmem, st, a,
+                    nullptr, true, di, KS::kStages);
+}
 template <int CB>
 static cudaError_t launch_codes(const CountArgs &a, const DevInfo &di, cudaStream_t st) {
   const unsigned g = grid_for(a.nchunks, (unsigned long long)di.count_sms);
   switch (a.width) {
-    case 8:
-      return launch_tma(pp_tma_kernel<8, PP_CAT_NCW, CB>, g, CatShape::kThreads, CatShape::kSmem,
-                        st, a, nullptr, true, di, CatShape::kStages);
-    case 16:
-      return launch_tma(pp_tma_kernel<16, PP_CAT_NCW, CB>, g, CatShape::kThreads,
-                        CatShape::kSmem, st, a, nullptr, true, di, CatShape::kStages);
-    case 32:
-      return launch_tma(pp_tma_kernel<32, PP_CAT_NCW, CB>, g, CatShape::kThreads,
-                        CatShape::kSmem, st, a, nullptr, true, di, CatShape::kStages);
-    default:
-      return launch_tma(pp_tma_kernel<64, PP_CAT_NCW, CB>, g, CatShape::kThreads,
-                        CatShape::kSmem, st, a, nullptr, true, di, CatShape::kStages);
+    case 8: return launch_codes_w<8, CB>(a, g, di, st);
+    case 16: return launch_codes_w<16, CB>(a, g, di, st);
+    case 32: return launch_codes_w<32, CB>(a, g, di, st);
+    default: return launch_codes_w<64, CB>(a, g, di, st);
   }
 }
 

@@ -45,6 +45,9 @@ struct CountArgs {
   // ticketed launches: trigger once tickets reach the last trigger_tail
   // chunks per CTA (0: after the CTA's last load)
   unsigned int trigger_tail;
+  // fused one-hot producer: bytes per row of the shared-memory one-hot table
+  // (pp_count.cu KShape; a kernel argument so the address is one IMAD)
+  unsigned int tab_mul;
   // checked builds (PP_CHECK_BOUNDS): the caller's byte range as the API
   // received it, and a per-launch {chunks consumed, CTAs finished} pair
   uintptr_t chk_lo, chk_hi;
