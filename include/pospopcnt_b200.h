@@ -123,9 +123,11 @@ PP_API int pp_count_sync(const void *data, size_t nbytes, int width,
  * HOST counters.  Synchronous.  Replaces the bytes-like path of pospopcnt()
  * (kernels.py:315-333 with data = bytes/bytearray/memoryview; cli.py:82-94).
  * Resources, per calling host thread and device, allocated on first use and
- * kept: 3 x 64 MiB device buffers (inputs > 1 MiB), 3 x 64 MiB pinned staging
- * buffers (pageable inputs >= 32 MiB only), 1 MiB pinned + 1 MiB device for
- * small inputs.
+ * kept: 3 x 64 MiB device buffers (inputs > 1 MiB), 3 x 16 MiB pinned staging
+ * buffers (pageable inputs >= 2 MiB: copied there in <= 8 MiB pieces by a pool
+ * of host threads with non-temporal stores, so the copy engine reads them from
+ * DRAM and not out of the cores' caches), 1 MiB pinned + 1 MiB device for small
+ * inputs.
  */
 PP_API int pp_count_host(const void *host_data, size_t nbytes, int width,
                   unsigned long long *host_counters);

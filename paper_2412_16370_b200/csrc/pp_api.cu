@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <emmintrin.h>
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
@@ -518,6 +519,37 @@ constexpr int kNbuf = 3;
 constexpr size_t kChunk = (size_t)PP_HOST_CHUNK_MIB << 20;
 
 // Parallel memcpy on a persistent pool; the calling thread works too.
+// memcpy into a pinned staging buffer with non-temporal stores (PP_HOST_NT=0:
+// plain memcpy).  The bytes are read next by the GPU's copy engine, not by
+// this CPU: left dirty in the cores' caches they make the DMA snoop every
+// line (the last chunk of a call, which nothing evicts, took 1.5 ms for
+// 8 MiB); streamed past the caches they are in DRAM when the DMA starts.
+inline void stage_copy(void *dst, const void *src, size_t n) {
+  static const bool nt = [] {
+    const char *e = std::getenv("PP_HOST_NT");
+    return !e || std::atoi(e) != 0;
+  }();
+  uint8_t *d = static_cast<uint8_t *>(dst);
+  const uint8_t *s = static_cast<const uint8_t *>(src);
+  if (!nt || ((uintptr_t)d & 15u) || n < 256) {
+    std::memcpy(d, s, n);
+    return;
+  }
+  size_t i = 0;
+  for (; i + 64 <= n; i += 64) {
+    const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i));
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i + 16));
+    const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i + 32));
+    const __m128i e = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i + 48));
+    _mm_stream_si128(reinterpret_cast<__m128i *>(d + i), a);
+    _mm_stream_si128(reinterpret_cast<__m128i *>(d + i + 16), b);
+    _mm_stream_si128(reinterpret_cast<__m128i *>(d + i + 32), c);
+    _mm_stream_si128(reinterpret_cast<__m128i *>(d + i + 48), e);
+  }
+  if (i < n) std::memcpy(d + i, s + i, n - i);
+  _mm_sfence();
+}
+
 class CopyPool {
  public:
   static CopyPool &get() {
@@ -525,8 +557,12 @@ class CopyPool {
     return *pool;
   }
   void copy(void *dst, const void *src, size_t n) {
-    if (workers_.empty() || n < (4u << 20)) {
-      std::memcpy(dst, src, n);
+    static const size_t pool_min = [] {  // PP_HOST_POOL_MIN: A/B of the threshold
+      const char *env = std::getenv("PP_HOST_POOL_MIN");
+      return env ? (size_t)std::strtoull(env, nullptr, 10) : (size_t)(1u << 20);
+    }();
+    if (workers_.empty() || n < pool_min) {
+      stage_copy(dst, src, n);
       return;
     }
     std::lock_guard<std::mutex> one_job(job_m_);
@@ -574,7 +610,7 @@ class CopyPool {
         s = src_ + off;
         len = std::min(piece_, n_ - off);
       }
-      std::memcpy(d, s, len);
+      stage_copy(d, s, len);
       std::lock_guard<std::mutex> lk(m_);
       if (--remaining_ == 0) done_cv_.notify_all();
     }
@@ -601,6 +637,7 @@ class CopyPool {
   uint64_t gen_ = 0;
 };
 
+constexpr size_t kStageMax = 16u << 20;  // pinned staging buffers (pageable inputs), each
 struct HostCtx {
   int dev = -1;
   cudaStream_t copy = nullptr, count = nullptr;
@@ -653,7 +690,7 @@ struct HostCtx {
   cudaError_t ensure_pinned() {
     cudaError_t e;
     for (int i = 0; i < kNbuf; ++i)
-      if (!pinned[i] && (e = cudaMallocHost(&pinned[i], kChunk))) return e;
+      if (!pinned[i] && (e = cudaMallocHost(&pinned[i], kStageMax))) return e;
     return cudaSuccess;
   }
 };
@@ -718,7 +755,7 @@ int count_small_host(SyncCtx &c, const void *host, size_t nbytes, int width,
   if (nbytes >= (256u << 10))
     CopyPool::get().copy(c.pin, host, nbytes);
   else
-    std::memcpy(c.pin, host, nbytes);
+    stage_copy(c.pin, host, nbytes);
   // same byte alignment on the device as on the host is not needed: counts
   // of a word-complete range do not depend on its address
   if ((e = cudaMemcpyAsync(c.dbuf, c.pin, nbytes, cudaMemcpyHostToDevice, c.st)))
@@ -783,12 +820,14 @@ int count_host_current(const void *host_data, size_t nbytes, int width,
   e = hc->ensure(dev);
   if (e != cudaSuccess) return cuda_fail(e, "pp_count_host setup");
   HostCtx &h = *hc;
-  // pageable sources of >= 32 MiB go through our pinned ring + parallel copy
-  // pool; below that the driver's own pageable path is as fast (both are
-  // host-memcpy-bound at 7-26 GB/s for 1-32 MiB: scripts/host_path_ab.py)
+  // pageable sources of >= 2 MiB go through our pinned ring + parallel copy
+  // pool (non-temporal stores, stage_copy): 2 / 4 / 8 / 16 / 32 / 256 MiB =
+  // 20 / 25 / 35 / 39 / 42 / 49 GB/s against 14 / 15 / 16 / 17 / 13 / 39 for
+  // the driver's own pageable path below 32 MiB and cached stores above
+  // (scripts/host_fixed_probe.py)
   static const size_t stage_min = [] {  // PP_HOST_STAGE_MIN: A/B of the threshold
     const char *env = std::getenv("PP_HOST_STAGE_MIN");
-    return env ? (size_t)std::strtoull(env, nullptr, 10) : (size_t)(32u << 20);
+    return env ? (size_t)std::strtoull(env, nullptr, 10) : (size_t)(2u << 20);
   }();
   const bool staged = nbytes >= stage_min && !host_is_pinned(host_data);
   // staged chunks are smaller so the pool copy of chunk i+1 overlaps the DMA
@@ -797,7 +836,7 @@ int count_host_current(const void *host_data, size_t nbytes, int width,
     const char *env = std::getenv("PP_HOST_STAGE_CHUNK");
     size_t c = env ? (size_t)std::strtoull(env, nullptr, 10) : (size_t)(8u << 20);
     c &= ~(size_t)63;
-    return (c < (1u << 20) || c > kChunk) ? (size_t)(8u << 20) : c;
+    return (c < (1u << 20) || c > kStageMax) ? (size_t)(8u << 20) : c;
   }();
   // a few chunks even for mid-size inputs, so the pool copy of chunk i + 1
   // overlaps the DMA of chunk i
