@@ -16,19 +16,22 @@ Printed JSON keys beyond the base contract:
   roofline       dominant kernel: algorithmic bytes per launch (n input bytes,
                  SURVEY.md 8d) / mean launch time vs MEASURED_PEAKS.hbm_gbs,
                  plus the in-run read-only roofline kernel and ncu traffic
-  cpu_baseline   the reference's fastest CPU path (C restatement of
-                 NumbaKernel.run, oracle/) on the host's cores, bounded sample
+  cpu_baseline   the reference's fastest CPU path on the host's cores, bounded
+                 sample: the unmodified reference (baseline/_ref, numba kernel
+                 on P forked processes) when it is installed, else the C
+                 restatement of NumbaKernel.run (oracle/)
   e2e            the same metric through the public API pospopcnt() on a
                  pinned HOST buffer: H2D copies + D2H of the counters inside
-                 the timed region
+                 the timed region; e2e_pageable: the same call on a pageable
+                 numpy array; e2e_fanout: one host buffer over every GPU
   exact          counters after all steps == steps x expected (CPU oracle, or
                  the reference's own golden totals for C3 codes / C5)
   per_width_gbs  C2 bytes counted at every word width (the metric is per w)
   clocks         NVML SM clock / throttle reasons sampled inside the region
 
-``--impl reference`` times the reference's CPU implementation (the oracle
-port; the reference itself is Python and is not on the GPU box) on the same
-config with all host threads.  ``--config`` selects another config (c1, c3,
+``--impl reference`` times the reference's CPU implementation (the unmodified
+reference from baseline/_ref on all host cores; the oracle's C port only when
+that install is absent) on the same config.  ``--config`` selects another config (c1, c3,
 c3cat, c4, c4seg, c5) for an extra line.
 """
 
@@ -929,6 +932,7 @@ def main_gpu(args):
 
     # e2e through the public API from pinned host memory
     e2e = None
+    e2e_pageable = None
     if args.e2e and seg_out is None and nbytes <= 4 * GIB:
         pinned = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
         pinned.copy_(buf[offset:offset + nbytes])
@@ -962,6 +966,21 @@ def main_gpu(args):
         e2e = {"value": round(world * nbytes * nst / t_e2e / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": w * 8,
                "path": e2e_path, "steps": nst}
+        if not use_dist and not categorical:
+            # the same call on PAGEABLE host memory (what the reference's
+            # callers pass: bytes / numpy arrays / a mapped file): staged
+            # through pinned pieces by the library's copy pool
+            pageable = pinned.numpy().copy()
+            pp.pospopcnt(pageable, w)
+            t0 = time.perf_counter()
+            for _ in range(nst):
+                res = pp.pospopcnt(pageable, w)
+            e2e_pageable = {"value": round(nbytes * nst / (time.perf_counter() - t0) / 1e9, 3),
+                            "unit": "GB/s", "steps": nst,
+                            "path": "pospopcnt(numpy array in pageable memory) -> pp_count_host: "
+                                    "<= 8 MiB pinned staging pieces filled by the host copy pool "
+                                    "(non-temporal stores), H2D and counting pipelined behind it"}
+            del pageable
         del pinned, res
     elif args.e2e and seg_out is not None:
         # segmented batch from host memory through the public API: the batch
@@ -1099,6 +1118,7 @@ def main_gpu(args):
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_pageable": e2e_pageable,
             "e2e_fanout": e2e_fanout,
             "strong_c5": strong_c5,
             "gpu_launches": args.steps,
