@@ -50,6 +50,8 @@ def test_bench_line_contract(cuda):
     assert e["unit"] == "GB/s" and e["value"] > 0
     assert e["h2d_bytes_per_step"] == d["config"]["bytes_per_gpu_per_step"]
     assert e["d2h_bytes_per_step"] > 0
+    # the same public call on pageable memory (bytes / numpy callers)
+    assert d["e2e_pageable"]["unit"] == "GB/s" and d["e2e_pageable"]["value"] > 0
     assert d["gpu_launches"] == 5
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert "workload" in d["config"]
