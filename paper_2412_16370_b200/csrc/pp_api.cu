@@ -4,7 +4,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#if defined(__x86_64__) || defined(_M_X64)
 #include <emmintrin.h>
+#define PP_HAVE_SSE2 1
+#else
+#define PP_HAVE_SSE2 0
+#endif
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
@@ -525,6 +530,9 @@ constexpr size_t kChunk = (size_t)PP_HOST_CHUNK_MIB << 20;
 // line (the last chunk of a call, which nothing evicts, took 1.5 ms for
 // 8 MiB); streamed past the caches they are in DRAM when the DMA starts.
 inline void stage_copy(void *dst, const void *src, size_t n) {
+#if !PP_HAVE_SSE2
+  std::memcpy(dst, src, n);  // (no streaming stores written for this host ISA)
+#else
   static const bool nt = [] {
     const char *e = std::getenv("PP_HOST_NT");
     return !e || std::atoi(e) != 0;
@@ -548,6 +556,7 @@ inline void stage_copy(void *dst, const void *src, size_t n) {
   }
   if (i < n) std::memcpy(d + i, s + i, n - i);
   _mm_sfence();
+#endif
 }
 
 class CopyPool {
