@@ -104,15 +104,18 @@ def load_traffic(kernel_key, input_bytes):
 
 
 def load_alu(kernel_key):
-    """ALU-pipe lane-instructions per input byte (= per u8 code) of a fused
-    producer kernel, from the committed ncu capture (profiles/ncu_alu.json)."""
+    """(ALU-pipe lane-instructions, shared-memory wavefronts) per input byte
+    (= per u8 code) of a fused producer kernel, from the committed ncu
+    capture (profiles/ncu_alu.json); None where absent."""
     p = os.path.join(ROOT, "profiles", "ncu_alu.json")
     try:
         with open(p) as f:
             d = json.load(f)[kernel_key]
-        return round(d["alu_warp_inst"] * 32 / d["input_bytes"], 4)
+        alu = round(d["alu_warp_inst"] * 32 / d["input_bytes"], 4)
+        lds = d.get("lds_wavefronts")
+        return alu, (lds / d["input_bytes"] if lds else None)
     except Exception:  # noqa: BLE001
-        return None
+        return None, None
 
 
 class ClockSampler:
@@ -910,7 +913,7 @@ def main_gpu(args):
         # the fused producer is ALU-bound, not HBM-bound (profiles/r2_cat_ncu.md):
         # ALU-pipe lane-ops per code (ncu, this build) x codes/s (live) against
         # 148 SMs x 64 lane-ops/clk x the SM clock sampled in the region
-        alu = load_alu(kernel_key)
+        alu, lds = load_alu(kernel_key)
         if alu is not None:
             mhz = clk.summary().get("sm_mhz") or 1965.0
             ops = alu * per_step_bytes / (k_ms / 1e3) / 1e12
@@ -920,6 +923,11 @@ def main_gpu(args):
                         "unit": "T lane-ops/s", "frac": round(ops / apeak, 4),
                         "traffic": traffic, "kernel": kernel_key,
                         "alu_lane_ops_per_code_ncu": alu,
+                        # the second pipe the kernel leans on: shared-memory
+                        # wavefronts (codes' LDS.U8 + table loads) against one
+                        # wavefront per clock per SM
+                        "smem_pipe_frac": (round(lds * per_step_bytes / (k_ms / 1e3)
+                                                 / (148 * mhz * 1e6), 4) if lds else None),
                         "peak_source": f"148 SMs x 64 ALU-pipe lane-ops/clk x {mhz:.0f} MHz "
                                        "(median SM clock in the timed region)",
                         "hbm": {k: hbm[k] for k in ("achieved", "peak", "unit", "frac",

@@ -70,34 +70,47 @@ struct TmaShape {
 #endif
 using CatShape = TmaShape<PP_CAT_NCW>;
 
-// One-hot words from a shared-memory table (u8 codes at W = 64): for
-// PP_CAT_TAB64 of every 16 codes of a chunk (a static share; 0 = off) the
-// (lo, hi) one-hot pair is LOADED from a per-lane table -- entry c of lane l
-// at c * 256 + l * 8 bytes: every lane has its own banks, so the loads are
-// conflict-free whatever the codes; entries c >= 64 are zero, so large codes
+// One-hot words from a shared-memory table (u8 codes at W = 32 / 64): for a
+// static share of the codes of a chunk -- PP_CAT_TAB64 of every 16 at W = 64,
+// PP_CAT_TAB32 of every 32 at W = 32; 0 = off -- the one-hot word (pair) is
+// LOADED from a per-lane table -- entry c of lane l at (c * 32 + l) * E
+// bytes, E = 8 / 4: every lane has its own banks, so the loads are
+// conflict-free whatever the codes; entries c >= W are zero, so large codes
 // and absent slots (0xFF) vanish -- at an address made by one IMAD, instead
-// of being computed by two ALU shifts.  The counter's LOP3s keep more of the
-// ALU pipe and the LSU / FMA pipes, mostly idle otherwise, carry part of the
-// one-hot step; the share balances the ALU pipe (3.1 - 1.0 f clk per 32
-// codes per SM) against the LSU (1 + 2 f): 11/16 measured best (0 / 6 / 8 /
-// 10 / 11 / 12 / 14 / 16 of 16 = 2806 / 3113 / 3196 / 3280 / 3291 / 3204 /
-// 2992 / 2803 G codes/s, scripts/gpu_cat_tab.sh).  The 64 KiB table takes
-// the third stage's shared memory: this kernel runs a 2-stage ring (no loss
-// at its 3.3 TB/s).  At W = 32 the same scheme (LDS.32 table, best share
-// 8/32) measured +1.3 % only, less than its 2-stage ring costs at 5.3 TB/s;
-// not kept.
+// of being computed on the ALU pipe (two shifts / one BMSK).  The counter's
+// LOP3s keep more of the ALU pipe and the LSU / FMA pipes, mostly idle
+// otherwise, carry part of the one-hot step; the share balances the ALU
+// pipe against the shared-memory data pipe (one wavefront per clock: the
+// codes' LDS.U8 1, LDS.64 2, LDS.32 1 per 32 codes).  W = 64 (ALU 3.1 - 1.0 f
+// vs LSU 1 + 2 f clocks per 32 codes per SM): 0 / 6 / 8 / 10 / 11 / 12 / 14 /
+// 16 of 16 = 2806 / 3113 / 3196 / 3280 / 3291 / 3204 / 2992 / 2803 G codes/s
+// (scripts/gpu_cat_tab.sh); its 64 KiB table takes the third stage's shared
+// memory, so it runs a 2-stage ring (no loss at 3.3 TB/s).  W = 32: 0 / 5 /
+// 7 / 9 / 11 / 13 of 32 = 5293 / 5370 / 5470 / 5570 / 5533 / 5494
+// (scripts/gpu_cat_tab32.sh); the 32 KiB table fits beside the 3-stage ring
+// once the epilogue's per-warp rows move into the ring (with a 2-stage ring
+// the same table gained 1.3 % only: the ring depth costs 2 % at 5.3 TB/s).
 #ifndef PP_CAT_TAB64
 #define PP_CAT_TAB64 11
 #endif
-#ifndef PP_CAT_TAB_STAGES
-#define PP_CAT_TAB_STAGES 2
+#ifndef PP_CAT_TAB32
+#define PP_CAT_TAB32 9
 #endif
 template <int MODE, int NCW, int CB>
 struct KShape {
   using Sh = TmaShape<NCW>;
-  static constexpr int kTabEntry = (CB == 1 && MODE == 64 && PP_CAT_TAB64 > 0) ? 8 : 0;
+  static constexpr int kTabEntry = (CB == 1 && MODE == 64 && PP_CAT_TAB64 > 0)   ? 8
+                                   : (CB == 1 && MODE == 32 && PP_CAT_TAB32 > 0) ? 4
+                                                                                 : 0;
   static constexpr int kTabBytes = 256 * 32 * kTabEntry;
-  static constexpr int kStages = kTabBytes ? PP_CAT_TAB_STAGES : Sh::kStages;
+  // the ring keeps its depth when the table fits beside it (W = 32: 192 + 32
+  // KiB, the epilogue's per-warp rows then live in the ring's last stage),
+  // else it gives up a stage (W = 64)
+  static constexpr bool kFits =
+      Sh::kStages * Sh::kStageBytes + 2 * Sh::kStages * 8 + 16 + kTabBytes + 1024 <= 227 * 1024;
+  static constexpr int kStages = (kTabBytes && !kFits) ? Sh::kStages - 1 : Sh::kStages;
+  // per-warp epilogue rows in the stage that carried the "no chunk" sentinel
+  static constexpr bool kRowsInStage = kTabBytes != 0;
   static constexpr size_t kBarOff = kStages * Sh::kStageBytes;
   static constexpr size_t kTabOff = (kBarOff + 2 * kStages * 8 + 15) & ~(size_t)15;
   static constexpr size_t kSmem = kTabOff + kTabBytes;
@@ -325,6 +338,12 @@ __device__ __forceinline__ uint32_t bit_at(uint32_t n) {
 // table entry of code c for this lane (tab = shared address of the lane's
 // column, mul = bytes per table row, a kernel argument so that the address
 // is one IMAD on the FMA pipe and not shifts/adds on the ALU pipe)
+__device__ __forceinline__ uint32_t tab_load32(uint32_t c, uint32_t mul, uint32_t tab) {
+  uint32_t addr, r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(c), "r"(mul), "r"(tab));
+  asm("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(addr));
+  return r;
+}
 __device__ __forceinline__ void tab_load64(uint32_t c, uint32_t mul, uint32_t tab, uint32_t &lo,
                                            uint32_t &hi) {
   uint32_t addr;
@@ -350,8 +369,12 @@ __device__ __forceinline__ void eat_lds8(Ctr &c, const uint8_t *sb, int lim, con
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int j = 32 * g + 4 * q;
-        u[q] = make_uint4(bit_at(code(j)), bit_at(code(j + 1)), bit_at(code(j + 2)),
-                          bit_at(code(j + 3)));
+        uint32_t wq[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          wq[e] = tab_slot(4 * q + e, 32, PP_CAT_TAB32) ? tab_load32(code(j + e), mul, tab)
+                                                        : bit_at(code(j + e));
+        u[q] = make_uint4(wq[0], wq[1], wq[2], wq[3]);
       }
       c.csa(u, g);
     }
@@ -532,7 +555,12 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + KS::kBarOff);
   uint64_t *empty = full + KS::kStages;
   __shared__ unsigned long long frame[PP_EPI_SLOTS ? 1 : 64];
-  __shared__ unsigned long long wframe[PP_EPI_SLOTS ? NCW : 1][64];  // per-warp frame rows
+  // per-warp frame rows of the epilogue; kernels whose table leaves no room
+  // keep them in the ring's stage that carried the sentinel instead (free by
+  // then: every warp released it before the producer could reuse it, and no
+  // copy is issued after the sentinel)
+  __shared__ unsigned long long wframe[(PP_EPI_SLOTS && !KS::kRowsInStage) ? NCW : 1][64];
+  unsigned long long (*rows)[64] = wframe;
   __shared__ unsigned long long chunk_id[KS::kStages];  // written before the stage's arrival
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -547,9 +575,14 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   if (!PP_EPI_SLOTS && threadIdx.x < 64) frame[threadIdx.x] = 0;
   if constexpr (KS::kTabBytes != 0) {  // per-lane one-hot tables (see KShape)
     for (uint32_t i = threadIdx.x; i < 256u * 32u; i += (NCW + 1) * 32) {
-      uint32_t lo, hi;
-      onehot64(i >> 5, lo, hi);  // entry i / 32, lane i % 32
-      reinterpret_cast<uint2 *>(smem + KS::kTabOff)[i] = make_uint2(lo, hi);
+      // entry i / 32, lane i % 32
+      if constexpr (KS::kTabEntry == 8) {
+        uint32_t lo, hi;
+        onehot64(i >> 5, lo, hi);
+        reinterpret_cast<uint2 *>(smem + KS::kTabOff)[i] = make_uint2(lo, hi);
+      } else {
+        reinterpret_cast<uint32_t *>(smem + KS::kTabOff)[i] = onehot32(i >> 5);
+      }
     }
   }
   __syncthreads();
@@ -760,9 +793,11 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       if (threadIdx.x == 0) PP_TL(4);
       c.finish(t);
       if (blockIdx.x == 0 && warp == 0) edge_count<kEdgeCB>(c, edge, a.width, t);
+      if (KS::kRowsInStage)
+        rows = reinterpret_cast<unsigned long long(*)[64]>(stages + stage * Sh::kStageVecs);
       if (PP_EPI_SLOTS) {  // one row per warp: plain stores, summed by the fold
-        wframe[warp][lane] = c.ce;
-        wframe[warp][32 + lane] = c.co;
+        rows[warp][lane] = c.ce;
+        rows[warp][32 + lane] = c.co;
       } else {  // u64 shared atomics (a CAS loop in SASS, 8 warps contending)
         atomicAdd(&frame[lane], c.ce);
         atomicAdd(&frame[32 + lane], c.co);
@@ -779,7 +814,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   if (threadIdx.x == 0) PP_TL(5);
   if (kCount) {
     if (PP_EPI_SLOTS)
-      fold_rows_to_counters<NCW>(wframe, a);
+      fold_rows_to_counters<NCW>(rows, a);  // (threads < 64 are consumers: their `rows`)
     else
       fold_frame_to_counters(frame, a);
   }
