@@ -90,17 +90,25 @@ using CatShape = TmaShape<PP_CAT_NCW>;
 // (scripts/gpu_cat_tab32.sh); the 32 KiB table fits beside the 3-stage ring
 // once the epilogue's per-warp rows move into the ring (with a 2-stage ring
 // the same table gained 1.3 % only: the ring depth costs 2 % at 5.3 TB/s).
+// W = 16 (two codes per word, the same 32-bit table; PP_CAT_TAB16 of every
+// 64 codes): 0 / 6 / 10 / 14 / 18 / 24 = 6207 / 6277 / 6318 / 6241 / 6112 /
+// 5756 (scripts/gpu_cat_tab16.sh) -- a small gain, the kernel is within 15 %
+// of the HBM roofline there.
 #ifndef PP_CAT_TAB64
 #define PP_CAT_TAB64 11
 #endif
 #ifndef PP_CAT_TAB32
 #define PP_CAT_TAB32 9
 #endif
+#ifndef PP_CAT_TAB16
+#define PP_CAT_TAB16 10
+#endif
 template <int MODE, int NCW, int CB>
 struct KShape {
   using Sh = TmaShape<NCW>;
   static constexpr int kTabEntry = (CB == 1 && MODE == 64 && PP_CAT_TAB64 > 0)   ? 8
                                    : (CB == 1 && MODE == 32 && PP_CAT_TAB32 > 0) ? 4
+                                   : (CB == 1 && MODE == 16 && PP_CAT_TAB16 > 0) ? 4
                                                                                  : 0;
   static constexpr int kTabBytes = 256 * 32 * kTabEntry;
   // the ring keeps its depth when the table fits beside it (W = 32: 192 + 32
@@ -409,7 +417,11 @@ __device__ __forceinline__ void eat_lds8(Ctr &c, const uint8_t *sb, int lim, con
           const int j = 64 * g + 8 * q + 2 * e;
           // low halves of the two one-hot words (codes 16..31 fall in the
           // dropped high halves): one PRMT
-          wq[e] = prmt(bit_at(code(j)), bit_at(code(j + 1)), 0x5410u);
+          const uint32_t b0 = tab_slot(8 * q + 2 * e, 64, PP_CAT_TAB16)
+                                  ? tab_load32(code(j), mul, tab) : bit_at(code(j));
+          const uint32_t b1 = tab_slot(8 * q + 2 * e + 1, 64, PP_CAT_TAB16)
+                                  ? tab_load32(code(j + 1), mul, tab) : bit_at(code(j + 1));
+          wq[e] = prmt(b0, b1, 0x5410u);
         }
         u[q] = make_uint4(wq[0], wq[1], wq[2], wq[3]);
       }
