@@ -257,12 +257,29 @@ template <bool FULL, class Ctr>
 __device__ __forceinline__ void eat_codes8(Ctr &c, const uint4 (&v)[8], uint32_t valid,
                                            const TC &t) {
   uint4 u[8];
+  // Does any code of the warp's chunk need the >= 8 mask?  One warp-uniform
+  // branch per chunk: a per-vector test compiled to predicated mask code
+  // that was issued for every word whether needed or not (2.95 ALU lane-ops
+  // per code with or without large codes); categories that all fit the
+  // width -- the usual case -- now skip it.
+  uint32_t any = 0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const bool big = ((v[i].x | v[i].y | v[i].z | v[i].w) & 0xF8F8F8F8u) != 0;
-    u[i] = make_uint4(onehot8x4(v[i].x, big), onehot8x4(v[i].y, big), onehot8x4(v[i].z, big),
-                      onehot8x4(v[i].w, big));
-    if (!FULL && !((valid >> i) & 1u)) u[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (int i = 0; i < 8; ++i) any |= v[i].x | v[i].y | v[i].z | v[i].w;
+  if (__any_sync(0xFFFFFFFFu, (any & 0xF8F8F8F8u) != 0)) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      u[i] = make_uint4(onehot8x4(v[i].x, true), onehot8x4(v[i].y, true),
+                        onehot8x4(v[i].z, true), onehot8x4(v[i].w, true));
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      u[i] = make_uint4(onehot8x4(v[i].x, false), onehot8x4(v[i].y, false),
+                        onehot8x4(v[i].z, false), onehot8x4(v[i].w, false));
+  }
+  if (!FULL) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (!((valid >> i) & 1u)) u[i] = make_uint4(0u, 0u, 0u, 0u);
   }
   c.csa(u, 0);
   c.end_chunk(t);
