@@ -850,18 +850,12 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   if (threadIdx.x == 0) PP_TL(6);
 }
 
-__global__ void __launch_bounds__(kLdgThreads)
-    pp_count_ldg_kernel(CountArgs a) {
-  __shared__ unsigned long long frame[64];
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x < 64) frame[threadIdx.x] = 0;
-  __syncthreads();
-  const TC t = make_tc(lane);
-  Counter c;
-  c.init();
+// One CTA's grid-stride pass over the body's chunks (chunk cta, cta + ncta, ...).
+__device__ __forceinline__ void ldg_eat_chunks(Counter &c, const CountArgs &a, const TC &t,
+                                               unsigned long long cta, unsigned long long ncta) {
   const uint4 *body = reinterpret_cast<const uint4 *>(a.body);
   const unsigned long long nvec = a.body_bytes >> 4;
-  for (unsigned long long ch = blockIdx.x; ch < a.nchunks; ch += gridDim.x) {
+  for (unsigned long long ch = cta; ch < a.nchunks; ch += ncta) {
     const unsigned long long base = ch * kLdgChunkVecs + threadIdx.x;
     uint4 v[8];
     if ((ch + 1) * kLdgChunkVecs <= nvec) {
@@ -881,6 +875,18 @@ __global__ void __launch_bounds__(kLdgThreads)
     }
     c.eat8(v, t);
   }
+}
+
+__global__ void __launch_bounds__(kLdgThreads)
+    pp_count_ldg_kernel(CountArgs a) {
+  __shared__ unsigned long long frame[64];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < 64) frame[threadIdx.x] = 0;
+  __syncthreads();
+  const TC t = make_tc(lane);
+  Counter c;
+  c.init();
+  ldg_eat_chunks(c, a, t, blockIdx.x, gridDim.x);
   c.finish(t);
   if (blockIdx.x == 0 && warp == 0)
     count_edges(c, a.head, a.head_bytes, a.tail, a.tail_bytes, lane, t, a.chk_lo, a.chk_hi);
@@ -888,6 +894,43 @@ __global__ void __launch_bounds__(kLdgThreads)
   atomicAdd(&frame[32 + lane], c.co);
   __syncthreads();
   fold_frame_to_counters(frame, a);
+}
+
+// Small synchronous calls (pp_count_sync, small pp_count_host): ONE CTA counts
+// the whole range -- device memory, or host memory it reads over the link
+// through its mapped pinned address -- and publishes the result itself:
+// out[j] = count of position j (plain stores into mapped pinned host memory,
+// not accumulated), then *flag = seq.  The host polls the flag instead of
+// queueing a counter memset, a D2H copy and a stream synchronisation.
+__global__ void __launch_bounds__(kLdgThreads)
+    pp_count_direct_kernel(CountArgs a, unsigned long long *out, unsigned int *flag,
+                           unsigned int seq) {
+  __shared__ unsigned long long frame[64];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < 64) frame[threadIdx.x] = 0;
+  __syncthreads();
+  const TC t = make_tc(lane);
+  Counter c;
+  c.init();
+  ldg_eat_chunks(c, a, t, 0, 1);
+  c.finish(t);
+  if (warp == 0)
+    count_edges(c, a.head, a.head_bytes, a.tail, a.tail_bytes, lane, t, a.chk_lo, a.chk_hi);
+  atomicAdd(&frame[lane], c.ce);
+  atomicAdd(&frame[32 + lane], c.co);
+  __syncthreads();
+  const int j = threadIdx.x, width = a.width;
+  if (j < width) {
+    unsigned long long s = 0;
+    for (int i = j; i < 64; i += width) s += frame[(i + a.rot) & 63];
+    *reinterpret_cast<volatile unsigned long long *>(out + j) = s;
+    __threadfence_system();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // every out[] store is ordered before the flag
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned int *>(flag) = seq;
+  }
 }
 
 // ------------------------------------------------------------------ host side
@@ -1249,6 +1292,12 @@ static cudaError_t launch_codes(const CountArgs &a, const DevInfo &di, cudaStrea
     case 32: return launch_codes_w<32, CB>(a, g, di, st);
     default: return launch_codes_w<64, CB>(a, g, di, st);
   }
+}
+
+cudaError_t launch_count_direct(const CountArgs &a, unsigned long long *out, unsigned int *flag,
+                                unsigned int seq, cudaStream_t st) {
+  pp_count_direct_kernel<<<1, kLdgThreads, 0, st>>>(a, out, flag, seq);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_count_codes(const CountArgs &a, int code_bytes, const DevInfo &di,

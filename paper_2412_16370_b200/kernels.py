@@ -90,13 +90,15 @@ def _host_u8(base, offset, nbytes):
         if not base.is_contiguous():
             raise ValueError("input tensor must be contiguous")
         return base.data_ptr() + offset, base
-    arr = base if isinstance(base, np.ndarray) else np.frombuffer(
-        memoryview(base).cast("B"), dtype=np.uint8)
     if isinstance(base, np.ndarray):
-        if not arr.flags.c_contiguous:
+        if not base.flags.c_contiguous:
             raise ValueError("input array must be C-contiguous")
-        arr = arr.reshape(-1).view(np.uint8)
-    return arr.ctypes.data + offset, arr
+        arr = base.reshape(-1).view(np.uint8)
+    elif type(base) in (bytes, bytearray):
+        arr = np.frombuffer(base, dtype=np.uint8)
+    else:
+        arr = np.frombuffer(memoryview(base).cast("B"), dtype=np.uint8)
+    return arr.__array_interface__["data"][0] + offset, arr
 
 
 def _device_scratch(device):
@@ -112,10 +114,13 @@ def _device_scratch(device):
 
 
 def _host_result():
-    """Per-thread u64[64] host buffer the C calls write results into."""
+    """Per-thread u64[64] host buffer the C calls add results into, zeroed,
+    and its address."""
     r = getattr(_tls, "result", None)
     if r is None:
-        r = _tls.result = np.zeros(W_MAX, dtype=np.uint64)
+        arr = np.zeros(W_MAX, dtype=np.uint64)
+        r = _tls.result = (arr, arr.ctypes.data)
+    r[0].fill(0)
     return r
 
 
@@ -138,8 +143,7 @@ def _add_into(counters, values, w):
         counters[:w] += torch.as_tensor(np.asarray(values[:w], dtype=np.int64)).to(
             counters.device, counters.dtype)
         return
-    for j in range(w):
-        v = int(values[j])
+    for j, v in enumerate(values[:w].tolist()):  # Python ints in one call
         if v:
             counters[j] += v
 
@@ -218,9 +222,8 @@ class B200Kernel:
                     _lib.check(lib.pp_count(ptr, view.nbytes, w, dc.data_ptr(), stream))
                 return counters
             # host-side counters: count, copy back and synchronise in one C call
-            vals = _host_result()
-            vals[:w] = 0
-            _lib.check(lib.pp_count_sync(ptr, view.nbytes, w, vals.ctypes.data, stream))
+            vals, vals_ptr = _host_result()
+            _lib.check(lib.pp_count_sync(ptr, view.nbytes, w, vals_ptr, stream))
         finally:
             if switch:
                 torch.cuda.set_device(prev)
@@ -229,22 +232,21 @@ class B200Kernel:
 
     def _run_host(self, lib, view, w, counters):
         ptr, keep = _host_u8(view.base, view.offset, view.nbytes)
-        out = _host_result()
-        out[:] = 0
+        out, out_ptr = _host_result()
         dev_idx = None
         if is_torch_tensor(counters) and counters.is_cuda:
             dev_idx = counters.device.index
         devs = _resolve_devices(self.devices)
         if devs is not None and (len(devs) > 1 or dev_idx is None):
             arr = (ctypes.c_int * len(devs))(*devs)
-            _lib.check(lib.pp_count_host_multi(ptr, view.nbytes, w, out.ctypes.data, arr,
+            _lib.check(lib.pp_count_host_multi(ptr, view.nbytes, w, out_ptr, arr,
                                                len(devs)))
         elif dev_idx is not None:
             import torch
             with torch.cuda.device(dev_idx):
-                _lib.check(lib.pp_count_host(ptr, view.nbytes, w, out.ctypes.data))
+                _lib.check(lib.pp_count_host(ptr, view.nbytes, w, out_ptr))
         else:
-            _lib.check(lib.pp_count_host(ptr, view.nbytes, w, out.ctypes.data))
+            _lib.check(lib.pp_count_host(ptr, view.nbytes, w, out_ptr))
         del keep
         _add_into(counters, out, w)
         return counters

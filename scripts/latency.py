@@ -28,7 +28,8 @@ def main():
     big = gen.generate("uniform", 64 << 20, 0xC1, device=dev)
     cnt = torch.zeros(64, dtype=torch.int64, device=dev)
     rows = []
-    for n in (8, 64, 1024, 4096, 65536, 1 << 20, 2 << 20, 16 << 20, 64 << 20):
+    for n in (8, 64, 1024, 4096, 16384, 32768, 65536, 131072, 262144, 1 << 20, 2 << 20, 16 << 20,
+              64 << 20):
         w = 16
         ptr = big.data_ptr() + 3 if n < (64 << 20) else big.data_ptr()
         nn = n if n < (64 << 20) else n
@@ -57,12 +58,32 @@ def main():
             pp.pospopcnt(view, w)
         t_api_list = (time.perf_counter() - t0) / kk
         host = big[:nn].cpu().numpy().tobytes()
+        pp.pospopcnt(host, w)  # first use of a path allocates its pinned buffers
         t0 = time.perf_counter()
         for _ in range(kk):
             pp.pospopcnt(host, w)
         t_api_bytes = (time.perf_counter() - t0) / kk
+        # the synchronous C-ABI calls without the Python layer: device bytes ->
+        # host counters (pp_count_sync), host bytes -> host counters (pp_count_host)
+        import ctypes
+        import numpy as np
+        hc = np.zeros(64, dtype=np.uint64)
+        hb = np.frombuffer(host, dtype=np.uint8)
+        for _ in range(3):
+            _lib.check(lib.pp_count_sync(ptr, nn, w, hc.ctypes.data, sp))
+            _lib.check(lib.pp_count_host(hb.ctypes.data, nn, w, hc.ctypes.data))
+        t0 = time.perf_counter()
+        for _ in range(kk):
+            _lib.check(lib.pp_count_sync(ptr, nn, w, hc.ctypes.data, sp))
+        t_sync = (time.perf_counter() - t0) / kk
+        t0 = time.perf_counter()
+        for _ in range(kk):
+            _lib.check(lib.pp_count_host(hb.ctypes.data, nn, w, hc.ctypes.data))
+        t_host = (time.perf_counter() - t0) / kk
         row = {"bytes": n, "device_us_per_launch": round(dev_us, 2),
                "c_abi_call_us": round(t_cabi * 1e6, 2),
+               "c_abi_sync_us": round(t_sync * 1e6, 2),
+               "c_abi_host_us": round(t_host * 1e6, 2),
                "api_device_counters_us": round(t_api_dev * 1e6, 2),
                "api_list_counters_us": round(t_api_list * 1e6, 2),
                "api_host_bytes_us": round(t_api_bytes * 1e6, 2),

@@ -10,7 +10,8 @@ recorded; pp_check_status reads the record.
 Reference contract: nothing outside the buffer is read (edges.py:1-10,
 pkg/tests/test_kernels.py:83-91).  The suites below -- exact-allocation
 edges, the c1 sweep, segmented/ragged/tiny/batch arrays, the golden vectors
-incl. 64 GiB C5, categories, and a 60 s randomised soak -- run on the
+incl. 64 GiB C5, categories, the direct small-call path, and a 60 s
+randomised soak -- run on the
 checked build; every process reports its record at exit (PP_CHECK_REPORT)
 and every record must be clean.  The negative test corrupts the launchers'
 derived ranges on purpose and shows the checks fire.
@@ -55,7 +56,8 @@ def test_checked_build_suites_clean(cuda, tmp_path):
          os.path.join(ROOT, "tests", "test_gpu_edges.py"),
          os.path.join(ROOT, "tests", "test_gpu_golden.py"),
          os.path.join(ROOT, "tests", "test_gpu_segmented.py"),
-         os.path.join(ROOT, "tests", "test_gpu_categories.py")],
+         os.path.join(ROOT, "tests", "test_gpu_categories.py"),
+         os.path.join(ROOT, "tests", "test_gpu_parity.py") + "::test_direct_small_calls"],
         capture_output=True, text=True, timeout=1500, cwd=ROOT, env=env)
     assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-2000:]
     res = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "fuzz.py"),

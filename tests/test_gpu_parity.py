@@ -550,3 +550,53 @@ def test_scheduler_slots_reused_by_new_streams(cuda, oracle):
         assert [int(x) for x in c.cpu()] == want
     for h, _ in streams + busy:
         rt.cudaStreamDestroy(h)
+
+
+def test_direct_small_calls(cuda, oracle, rng):
+    """Synchronous small calls take the direct path (pp_count_direct_kernel:
+    one CTA reads the bytes in place -- host bytes through the pinned
+    small-call buffer over the link -- and publishes counts + a flag in
+    mapped pinned memory the host polls).  Sizes around its chunk (32 KiB)
+    and cut-off (256 KiB) boundaries, every width, odd offsets, both entry
+    points (pp_count_sync via list counters, pp_count_host via host bytes),
+    accumulate semantics, and many calls back to back (the flag's sequence
+    number must never let a call read its predecessor's counts)."""
+    torch, pp = cuda
+    K = 1 << 10
+    data = rng.randbytes(300 * K)
+    host = np.frombuffer(data, np.uint8)
+    buf = torch.from_numpy(host.copy()).cuda()
+    sizes = [8, 64, 4 * K, 32 * K - 16, 32 * K, 32 * K + 16, 64 * K + 8, 128 * K,
+             256 * K - 8, 256 * K, 256 * K + 8]
+    for w in (8, 16, 32, 64):
+        for n in sizes:
+            for off in (0, 3, 13):
+                want = oracle.hs512(host, off, n, w)
+                assert pp.pospopcnt(pp.InputView(buf, off, n), w) == want, ("sync", w, n, off)
+                assert pp.pospopcnt(data[off:off + n], w) == want, ("host", w, n, off)
+    c = [5] * 16
+    want = oracle.hs512(host, 1, 1000, 16)
+    pp.pospopcnt(pp.InputView(buf, 1, 1000), 16, counters=c)
+    pp.pospopcnt(data[1:1001], 16, counters=c)
+    assert c == [5 + 2 * v for v in want]
+    # back to back, alternating inputs: each call returns its own counts
+    wants = [oracle.hs512(host, 64 * i, 512 + 8 * i, 8) for i in range(8)]
+    for rep in range(300):
+        i = rep % 8
+        assert pp.pospopcnt(pp.InputView(buf, 64 * i, 512 + 8 * i), 8) == wants[i]
+        assert pp.pospopcnt(data[64 * i:64 * i + 512 + 8 * i], 8) == wants[i]
+    # a second stream and a second thread have their own publish slots
+    import threading
+    errs = []
+
+    def worker(k):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for rep in range(200):
+                i = (rep + k) % 8
+                if pp.pospopcnt(pp.InputView(buf, 64 * i, 512 + 8 * i), 8) != wants[i]:
+                    errs.append((k, rep))
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(3)]
+    [t.start() for t in ts]
+    [t.join() for t in ts]
+    assert not errs
