@@ -525,20 +525,37 @@ def test_scheduler_slots_reused_by_new_streams(cuda, oracle):
     busy = _raw_streams(300)
     # every stream waits on one host-released gate: all their launches are
     # in flight at once, so every slot is busy and the later ones must take
-    # the static order
+    # the static order.  The gate is a stream wait on a pinned host word
+    # (cuStreamWaitValue32) that this thread sets once the launches are
+    # queued -- no race against a timed blocker kernel.
+    from cuda.bindings import driver as drv
+    word = torch.zeros(1, dtype=torch.int32).pin_memory()
     gate = torch.cuda.Event()
     blocker = torch.cuda.Stream()
-    with torch.cuda.stream(blocker):
-        torch.cuda._sleep(int(2e9))  # ~1 s of device time
-        gate.record(blocker)
+    err, = drv.cuStreamWaitValue32(blocker.cuda_stream, word.data_ptr(), 1,
+                                   drv.CUstreamWaitValue_flags.CU_STREAM_WAIT_VALUE_EQ)
+    assert err == drv.CUresult.CUDA_SUCCESS, err
     outs = []
-    for h, s in busy:
-        s.wait_event(gate)
-        with torch.cuda.stream(s):
-            c = torch.zeros(8, dtype=torch.int64, device="cuda")
-            pp.pospopcnt(buf, 8, counters=c)
-        outs.append((s, c))
-    s2 = _sched_stats()
+    import threading
+
+    def release():
+        word[0] = 1
+    watchdog = threading.Timer(30.0, release)  # a blocked host call must not hang the GPU
+    watchdog.daemon = True
+    watchdog.start()
+    try:
+        gate.record(blocker)
+        for h, s in busy:
+            s.wait_event(gate)
+            with torch.cuda.stream(s):
+                c = torch.zeros(8, dtype=torch.int64, device="cuda")
+                pp.pospopcnt(buf, 8, counters=c)
+            outs.append((s, c))
+        s2 = _sched_stats()
+        assert not gate.query()  # still closed: every queued launch is pending
+    finally:
+        release()  # open the gate whatever happened above
+        watchdog.cancel()
     assert s2[2] > s1[2], (s1, s2)  # all-busy launches used the static order
     for s in keep:  # streams whose slots were taken over
         with torch.cuda.stream(s):
