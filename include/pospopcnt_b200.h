@@ -131,7 +131,7 @@ PP_API int pp_count_sync(const void *data, size_t nbytes, int width,
  * buffers (pageable inputs >= 2 MiB: copied there in <= 8 MiB pieces by a pool
  * of host threads with non-temporal stores, so the copy engine reads them from
  * DRAM and not out of the cores' caches), 1 MiB pinned + 1 MiB device for small
- * inputs.  Inputs up to 256 KiB are copied into that pinned buffer and
+ * inputs.  Inputs up to 128 KiB are copied into that pinned buffer and
  * counted in place by one CTA reading it over the link (the direct path of
  * pp_count_sync: no H2D copy either; 8 B..4 KiB 23 -> 18.5 us, 32 KiB 33 ->
  * 20.5 us per call).

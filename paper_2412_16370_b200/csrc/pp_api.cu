@@ -735,11 +735,13 @@ constexpr size_t kSmallHost = 1u << 20;
 // flag into mapped pinned memory that the host polls: one launch per call
 // instead of memset + launch + D2H copy + stream synchronisation (and, for
 // host bytes, the H2D copy).  A/B: PP_NO_DIRECT=1.
-// C-ABI call time, direct vs queued (scripts/gpu_direct_ab.sh): host bytes
-// 8 B..4 KiB 23 -> 18.5 us, 32 KiB 33 -> 20.5, 256 KiB 45 -> 40 (1 MiB: 78 vs
-// 109, so not there); device bytes -> host counters 19.5 -> 14.3 us up to
-// 64 KiB, 256 KiB 19.5 -> 17.5 (1 MiB: 19 vs 27.5).
-constexpr size_t kDirectHost = 256u << 10;
+// C-ABI call time, queued -> direct (scripts/gpu_direct_ab.sh, two boxes):
+// host bytes 8 B..4 KiB 23-27 -> 18.5-20.5 us, 16-32 KiB 33-40 -> 20-23,
+// 128 KiB 39-41 -> 30-36; 256 KiB 47 -> 41.5 on one box but 47 -> 49.5 on
+// the other (one CTA keeps 32 KiB of link reads in flight), so host bytes
+// stop at 128 KiB.  Device bytes -> host counters 19.5-22 -> 14.4-16 us up to
+// 64 KiB, 256 KiB 19.5-22.9 -> 17.9-19.9 (1 MiB: 19 vs 27.5).
+constexpr size_t kDirectHost = 128u << 10;
 constexpr size_t kDirectDevice = 256u << 10;
 struct SyncCtx {
   int dev = -1;

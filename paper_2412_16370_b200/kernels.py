@@ -84,6 +84,15 @@ class KernelDescriptor:
 _tls = threading.local()
 
 
+def _current_stream_handle(torch, dev):
+    """The current stream of ``dev`` as a raw cudaStream_t value (the fast
+    private accessor when this torch has it: ~1.5 us less per call)."""
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return raw(dev.index)
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
 def _host_u8(base, offset, nbytes):
     """(pointer, keepalive) for a host buffer slice."""
     if is_torch_tensor(base):
@@ -211,7 +220,7 @@ class B200Kernel:
             prev = torch.cuda.current_device()
             torch.cuda.set_device(dev)
         try:
-            stream = torch.cuda.current_stream(dev).cuda_stream
+            stream = _current_stream_handle(torch, dev)
             ptr = base.data_ptr() + view.offset
             dc = _device_counters(counters, w, dev)
             if dc is not None:
