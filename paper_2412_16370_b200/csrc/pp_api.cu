@@ -809,6 +809,13 @@ int count_direct(SyncCtx &c, const void *data, size_t nbytes, int width, unsigne
   if (e != cudaSuccess) return cuda_fail(e, "pp_count launch");
   volatile unsigned int *f = c.flag;
   for (unsigned spins = 1; *f != seq; ++spins) {
+    if (spins == (1u << 16)) {
+      // a few milliseconds without a result (the stream or the GPU is busy
+      // with other work): stop burning the core, wait the stream's way
+      if ((e = cudaStreamSynchronize(st))) return cuda_fail(e, "direct count");
+      if (*f == seq) break;
+      return fail(PP_ECUDA, "direct count finished without publishing its result");
+    }
     if ((spins & 0x3FFu) == 0) {
       e = cudaStreamQuery(st);
       if (e == cudaSuccess) {

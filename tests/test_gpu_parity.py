@@ -602,6 +602,9 @@ def test_direct_small_calls(cuda, oracle, rng):
         i = rep % 8
         assert pp.pospopcnt(pp.InputView(buf, 64 * i, 512 + 8 * i), 8) == wants[i]
         assert pp.pospopcnt(data[64 * i:64 * i + 512 + 8 * i], 8) == wants[i]
+    # a busy stream: the bounded poll gives way to a stream wait
+    torch.cuda._sleep(int(1e8))  # ~50 ms of device time ahead of the count
+    assert pp.pospopcnt(pp.InputView(buf, 64, 520), 8) == wants[1]
     # a second stream and a second thread have their own publish slots
     import threading
     errs = []
