@@ -112,11 +112,12 @@ PP_API int pp_count_ex(const void *data, size_t nbytes, int width,
  * counters: one call = zero a per-thread device scratch, count, copy the w
  * counters back, synchronise `stream`.  The reference's list-returning call
  * shape (kernels.py:315-333: pospopcnt(view, w) -> counters) for data that
- * already lives in HBM, without a caller-side D2H.  Up to 256 KiB the call is
- * ONE launch: a single CTA counts the range and writes the w counts and a
- * sequence flag into mapped pinned host memory, which the calling thread
- * polls (no memset, D2H copy or stream synchronisation: 19.5 -> 14.3 us per
- * call; the reference's short arrays, edges.py:96-102 count_short).
+ * already lives in HBM, without a caller-side D2H.  Up to 16 MiB the call is
+ * ONE launch: one CTA per 32 KiB counts the range and the kernel itself
+ * writes the w counts and a sequence flag into mapped pinned host memory,
+ * which the calling thread polls (no memset, D2H copy or stream
+ * synchronisation: 19.5 -> 14.4-15.5 us per call up to 4 MiB; the reference's
+ * short arrays, edges.py:96-102 count_short).
  */
 PP_API int pp_count_sync(const void *data, size_t nbytes, int width,
                          unsigned long long *host_counters, void *stream);
@@ -131,10 +132,10 @@ PP_API int pp_count_sync(const void *data, size_t nbytes, int width,
  * buffers (pageable inputs >= 2 MiB: copied there in <= 8 MiB pieces by a pool
  * of host threads with non-temporal stores, so the copy engine reads them from
  * DRAM and not out of the cores' caches), 1 MiB pinned + 1 MiB device for small
- * inputs.  Inputs up to 128 KiB are copied into that pinned buffer and
- * counted in place by one CTA reading it over the link (the direct path of
+ * inputs.  Inputs up to 512 KiB are copied into that pinned buffer and
+ * counted in place by CTAs reading it over the link (the direct path of
  * pp_count_sync: no H2D copy either; 8 B..4 KiB 23 -> 18.5 us, 32 KiB 33 ->
- * 20.5 us per call).
+ * 20.5, 256 KiB 44.5 -> 34-37 us per call).
  */
 PP_API int pp_count_host(const void *host_data, size_t nbytes, int width,
                   unsigned long long *host_counters);

@@ -729,23 +729,26 @@ bool is_device_memory(const void *p) {
 // a 1 MiB device buffer and a stream, so a small pp_count_host is one
 // memcpy + five stream operations + one synchronisation.
 constexpr size_t kSmallHost = 1u << 20;
-// Inputs up to kDirect bytes take the direct path (pp_count_direct_kernel):
-// one CTA reads the bytes where they are -- device memory, or the pinned
-// small-call buffer over the link -- and writes the counts and a sequence
-// flag into mapped pinned memory that the host polls: one launch per call
-// instead of memset + launch + D2H copy + stream synchronisation (and, for
-// host bytes, the H2D copy).  A/B: PP_NO_DIRECT=1.
-// C-ABI call time, queued -> direct (scripts/gpu_direct_ab.sh, two boxes):
-// host bytes 8 B..4 KiB 23-27 -> 18.5-20.5 us, 16-32 KiB 33-40 -> 20-23,
-// 128 KiB 39-41 -> 30-36; 256 KiB 47 -> 41.5 on one box but 47 -> 49.5 on
-// the other (one CTA keeps 32 KiB of link reads in flight), so host bytes
-// stop at 128 KiB.  Device bytes -> host counters 19.5-22 -> 14.4-16 us up to
-// 64 KiB, 256 KiB 19.5-22.9 -> 17.9-19.9 (1 MiB: 19 vs 27.5).
-constexpr size_t kDirectHost = 128u << 10;
-constexpr size_t kDirectDevice = 256u << 10;
+// Small and mid-size synchronous calls take the direct path
+// (pp_count_direct_kernel / pp_count_direct_multi_kernel): one CTA per 32 KiB
+// chunk reads the bytes where they are -- device memory, or the pinned
+// small-call buffer over the link -- and the kernel itself writes the counts
+// and a sequence flag into mapped pinned memory that the host polls: one
+// launch per call instead of memset + launch + D2H copy + stream
+// synchronisation (and, for host bytes, the H2D copy).  A/B: PP_NO_DIRECT=1,
+// PP_DIRECT_HOST_MAX / PP_DIRECT_DEVICE_MAX (scripts/gpu_direct_ab.sh).
+// C-ABI call time, queued -> direct: device bytes -> host counters 19-20 ->
+// 14.4-15.5 us up to 4 MiB, 16 MiB 25.4-26.4 -> 17.7-18.7 (above that the
+// TMA kernel's stream rate matters more than the saved operations); host
+// bytes 8 B..4 KiB 23-27 -> 18.5-20.5 us, 16-32 KiB 33-38 -> 20-21, 128 KiB
+// 39 -> 26-27.5, 256 KiB 44.5 -> 34-37, 512 KiB 57.8 -> 47-52 (1 MiB: 77-79
+// vs 75-83, a wash, so host bytes stop at 512 KiB).
+constexpr size_t kDirectHost = 512u << 10;
+constexpr size_t kDirectDevice = 16u << 20;
 struct SyncCtx {
   int dev = -1;
   unsigned long long *dcnt = nullptr, *hcnt = nullptr;
+  unsigned long long *acc = nullptr;       // direct path: 64 sums + a ticket, zero between calls
   unsigned long long *hcnt_dev = nullptr;  // hcnt / flag as the device addresses them
   unsigned int *flag = nullptr, *flag_dev = nullptr;
   unsigned int seq = 0;
@@ -755,6 +758,10 @@ struct SyncCtx {
     if (dev == d) return cudaSuccess;
     cudaError_t e;
     if (!dcnt && (e = cudaMalloc(&dcnt, 64 * sizeof(unsigned long long)))) return e;
+    if (!acc) {
+      if ((e = cudaMalloc(&acc, 65 * sizeof(unsigned long long)))) return e;
+      if ((e = cudaMemset(acc, 0, 65 * sizeof(unsigned long long)))) return e;
+    }
     if (!hcnt) {  // 64 counters + the flag word, mapped
       if ((e = cudaHostAlloc(&hcnt, 65 * sizeof(unsigned long long), cudaHostAllocMapped)))
         return e;
@@ -805,7 +812,7 @@ int count_direct(SyncCtx &c, const void *data, size_t nbytes, int width, unsigne
                   pp::count_chunk_bytes(pp::LoadPath::kLdg), &a);
   a.width = width;
   const unsigned int seq = ++c.seq ? c.seq : ++c.seq;  // never 0 (the initial flag)
-  cudaError_t e = pp::launch_count_direct(a, c.hcnt_dev, c.flag_dev, seq, st);
+  cudaError_t e = pp::launch_count_direct(a, c.acc, c.hcnt_dev, c.flag_dev, seq, st);
   if (e != cudaSuccess) return cuda_fail(e, "pp_count launch");
   volatile unsigned int *f = c.flag;
   for (unsigned spins = 1; *f != seq; ++spins) {

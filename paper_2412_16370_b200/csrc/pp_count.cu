@@ -933,6 +933,57 @@ __global__ void __launch_bounds__(kLdgThreads)
   }
 }
 
+// The same publish for ranges of several chunks: one CTA per 32 KiB chunk
+// (grid-stride beyond the grid), every CTA adds its folded counts into the
+// zeroed device scratch acc[0..63]; the CTA that draws the last ticket
+// (acc[64]) moves the totals to out[], leaves the scratch zeroed for the
+// next call and writes the flag.
+__global__ void __launch_bounds__(kLdgThreads)
+    pp_count_direct_multi_kernel(CountArgs a, unsigned long long *acc, unsigned long long *out,
+                                 unsigned int *flag, unsigned int seq) {
+  __shared__ unsigned long long frame[64];
+  __shared__ int last;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < 64) frame[threadIdx.x] = 0;
+  __syncthreads();
+  const TC t = make_tc(lane);
+  Counter c;
+  c.init();
+  ldg_eat_chunks(c, a, t, blockIdx.x, gridDim.x);
+  c.finish(t);
+  if (blockIdx.x == 0 && warp == 0)
+    count_edges(c, a.head, a.head_bytes, a.tail, a.tail_bytes, lane, t, a.chk_lo, a.chk_hi);
+  atomicAdd(&frame[lane], c.ce);
+  atomicAdd(&frame[32 + lane], c.co);
+  __syncthreads();
+  const int j = threadIdx.x, width = a.width;
+  if (j < width) {
+    unsigned long long s = 0;
+    for (int i = j; i < 64; i += width) s += frame[(i + a.rot) & 63];
+    if (s) atomicAdd(acc + j, s);
+    __threadfence();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(acc + 64, 1ull) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (j < width) {
+    const unsigned long long v = atomicExch(acc + j, 0ull);
+    *reinterpret_cast<volatile unsigned long long *>(out + j) = v;
+    __threadfence_system();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    acc[64] = 0;  // the next launch on any stream of this thread starts from zero
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned int *>(flag) = seq;
+  }
+}
+
 // ------------------------------------------------------------------ host side
 void split_range(const uint8_t *data, unsigned long long nbytes,
                  unsigned long long chunk_bytes, CountArgs *a) {
@@ -1294,9 +1345,15 @@ static cudaError_t launch_codes(const CountArgs &a, const DevInfo &di, cudaStrea
   }
 }
 
-cudaError_t launch_count_direct(const CountArgs &a, unsigned long long *out, unsigned int *flag,
-                                unsigned int seq, cudaStream_t st) {
-  pp_count_direct_kernel<<<1, kLdgThreads, 0, st>>>(a, out, flag, seq);
+cudaError_t launch_count_direct(const CountArgs &a, unsigned long long *acc,
+                                unsigned long long *out, unsigned int *flag, unsigned int seq,
+                                cudaStream_t st) {
+  if (a.nchunks <= 1) {
+    pp_count_direct_kernel<<<1, kLdgThreads, 0, st>>>(a, out, flag, seq);
+  } else {
+    const unsigned g = (unsigned)std::min<unsigned long long>(a.nchunks, 128);
+    pp_count_direct_multi_kernel<<<g, kLdgThreads, 0, st>>>(a, acc, out, flag, seq);
+  }
   return cudaGetLastError();
 }
 

@@ -143,11 +143,14 @@ unsigned long long count_chunk_bytes(LoadPath path);
 unsigned long long codes8_chunk_bytes();
 cudaError_t launch_count(const CountArgs &a, LoadPath path, const DevInfo &di,
                          cudaStream_t st);
-// one CTA counts the whole range (split with the LDG chunk size) and writes
-// out[j] (j < a.width, not accumulated) then *flag = seq, both in mapped
-// pinned host memory; a.counters is unused
-cudaError_t launch_count_direct(const CountArgs &a, unsigned long long *out, unsigned int *flag,
-                                unsigned int seq, cudaStream_t st);
+// the range (split with the LDG chunk size) counted by one CTA per chunk,
+// the result published by the kernel itself: out[j] (j < a.width, not
+// accumulated) then *flag = seq, both in mapped pinned host memory.  acc:
+// 65 zeroed u64 of device scratch (left zeroed), used when the range has
+// more than one chunk.  a.counters is unused.
+cudaError_t launch_count_direct(const CountArgs &a, unsigned long long *acc,
+                                unsigned long long *out, unsigned int *flag, unsigned int seq,
+                                cudaStream_t st);
 cudaError_t launch_segmented(const SegArgs &a, const DevInfo &di, cudaStream_t st);
 // fused one-hot producer over 1/2/4-byte codes (a.width = W, a.rot ignored)
 cudaError_t launch_count_codes(const CountArgs &a, int code_bytes, const DevInfo &di,

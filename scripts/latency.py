@@ -28,7 +28,8 @@ def main():
     big = gen.generate("uniform", 64 << 20, 0xC1, device=dev)
     cnt = torch.zeros(64, dtype=torch.int64, device=dev)
     rows = []
-    for n in (8, 64, 1024, 4096, 16384, 32768, 65536, 131072, 262144, 1 << 20, 2 << 20, 16 << 20,
+    for n in (8, 64, 1024, 4096, 16384, 32768, 65536, 131072, 262144, 524288, 1 << 20, 2 << 20, 4 << 20,
+              16 << 20,
               64 << 20):
         w = 16
         ptr = big.data_ptr() + 3 if n < (64 << 20) else big.data_ptr()

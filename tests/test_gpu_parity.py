@@ -573,18 +573,21 @@ def test_direct_small_calls(cuda, oracle, rng):
     """Synchronous small calls take the direct path (pp_count_direct_kernel:
     one CTA reads the bytes in place -- host bytes through the pinned
     small-call buffer over the link -- and publishes counts + a flag in
-    mapped pinned memory the host polls).  Sizes around its chunk (32 KiB)
-    and cut-off (128 KiB host, 256 KiB device) boundaries, every width, odd offsets, both entry
+    mapped pinned memory the host polls; ranges of several chunks: one CTA
+    per chunk, the last one publishes).  Sizes around its chunk (32 KiB) and
+    cut-off (512 KiB host, 16 MiB device) boundaries, every width, odd offsets, both entry
     points (pp_count_sync via list counters, pp_count_host via host bytes),
     accumulate semantics, and many calls back to back (the flag's sequence
     number must never let a call read its predecessor's counts)."""
     torch, pp = cuda
     K = 1 << 10
-    data = rng.randbytes(300 * K)
+    data = rng.randbytes(16500 * K)
     host = np.frombuffer(data, np.uint8)
     buf = torch.from_numpy(host.copy()).cuda()
     sizes = [8, 64, 4 * K, 32 * K - 16, 32 * K, 32 * K + 16, 64 * K + 8, 128 * K - 8, 128 * K,
-             128 * K + 8, 256 * K - 8, 256 * K, 256 * K + 8]
+             128 * K + 8, 256 * K + 8,
+             512 * K - 8, 512 * K, 512 * K + 8, 1024 * K + 8, 4096 * K + 64, 16384 * K - 8,
+             16384 * K, 16384 * K + 8]
     for w in (8, 16, 32, 64):
         for n in sizes:
             for off in (0, 3, 13):
